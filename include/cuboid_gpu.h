@@ -1,0 +1,163 @@
+/*
+ * cuboid_gpu.h -- C ABI of the B200 (sm_100a) residue-table builder and (p,q)
+ * pair sieve for the modulo-primes perfect-cuboid search (arXiv 1601.00636).
+ *
+ * The reference (/root/reference/proj) is a header-only C++20 library with no
+ * FFI; the drop-in points this ABI replaces are (paths relative to
+ * /root/reference/proj):
+ *
+ *   build_table(r)                 include/cuboid/sievetable.hpp:123-141
+ *   build_table_oracle(r)          include/cuboid/sievetable.hpp:102-115
+ *   SieveSet::build(primes)        include/cuboid/sievetable.hpp:159-176
+ *   load_sieve(tables, index)      include/cuboid/sievetable.hpp:254-292
+ *   scan(set, start, p_end, ...)   include/cuboid/engine.hpp:195-295
+ *   ScanStats / ScanSink           include/cuboid/engine.hpp:97-135
+ *
+ * Plain pointers and sizes only; no exceptions cross this boundary. Every
+ * function returns a cgpu_status: 0 on success, the reference's own scan status
+ * codes 2..6 (engine.hpp:5-12) where it would throw ScanRejected{code}, and
+ * negative values where it would throw another exception or where CUDA fails.
+ * cgpu_last_error() returns a thread-local message for the last failure.
+ *
+ * Table bytes are ALWAYS the reference's packed format: per prime r, ceil(r^2/8)
+ * bytes, bit i = a*r + b at byte i>>3, bit i&7 (LSB first), 1 = "Q_ab(t) has no
+ * root mod r"; tables concatenated at cumulative byte offsets
+ * (sievetable.hpp:1-19, 41-64).
+ */
+#ifndef CUBOID_GPU_H
+#define CUBOID_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+	CGPU_OK = 0,
+	/* 2..6: ScanRejected codes of the reference (engine.hpp:5-12, 152-161) */
+	CGPU_P_BELOW_152 = 2,
+	CGPU_P_ABOVE_LIMIT = 3,
+	CGPU_Q_BELOW_LOW = 4,
+	CGPU_Q_ABOVE_HIGH = 5,
+	CGPU_NOT_LOADED = 6,
+	CGPU_ERR_CUDA = -1,          /* CUDA runtime failure (see cgpu_last_error) */
+	CGPU_ERR_INVALID = -2,       /* std::invalid_argument in the reference */
+	CGPU_ERR_OVERFLOW = -3,      /* std::overflow_error (set exceeds 2^32 bytes) */
+	CGPU_ERR_FORMAT = -4,        /* FormatError (sievetable.hpp:37-39) */
+	CGPU_ERR_RANGE = -5,         /* std::out_of_range */
+	CGPU_ERR_CAPACITY = -6,      /* caller's output buffer too small; sizes still reported */
+	CGPU_ERR_NO_DEVICE = -7      /* no CUDA device: this library has no CPU fallback */
+} cgpu_status;
+
+/* Row-bound modes of the sieve. REGION = the reference scan() region
+ * q_low(p) <= q <= 59p (region.hpp:49-63, engine.hpp:225-227). TRIANGLE =
+ * 1 <= q < p (the BASELINE configs; loop of verify_small_region,
+ * engine.hpp:613-625). The filter is identical: skip q == p and gcd > 1
+ * (engine.hpp:258). */
+enum { CGPU_REGION = 0, CGPU_TRIANGLE = 1 };
+
+/* Table-build algorithms. PRODUCTION = build_table's row-1 + permutation
+ * (sievetable.hpp:123-141). EXHAUSTIVE = the definition over every
+ * (a,b,t) in Z_r^3 (sievetable.hpp:102-115, without early exit): exactly
+ * sum r^3 Q evaluations. Both emit byte-identical tables. */
+enum { CGPU_BUILD_PRODUCTION = 0, CGPU_BUILD_EXHAUSTIVE = 1 };
+
+typedef struct cgpu_ctx cgpu_ctx;
+
+const char* cgpu_last_error(void);
+const char* cgpu_version(void);
+
+/* One context per device (one process per GPU). `stream` may be NULL (the
+ * context creates its own) or a cudaStream_t owned by the caller. */
+int cgpu_create(int device, void* stream, cgpu_ctx** out);
+int cgpu_destroy(cgpu_ctx* ctx);
+int cgpu_set_stream(cgpu_ctx* ctx, void* stream);
+int cgpu_synchronize(cgpu_ctx* ctx);
+
+/* ---- tables ------------------------------------------------------------ */
+
+/* Size query mirroring SieveSet::build's validation (sievetable.hpp:159-176):
+ * strictly increasing primes below 9697, total bytes below 2^32. Fills
+ * offsets[n] (may be NULL) and *total_bytes. Host-only. */
+int cgpu_table_layout(const uint32_t* primes, uint32_t n, uint32_t* offsets, uint64_t* total_bytes);
+
+/* Builds the set for `primes` ON THE DEVICE and keeps it resident in ctx
+ * (replaces SieveSet::build). If out_bytes != NULL the packed tables
+ * (total_bytes of cgpu_table_layout) are copied back; out_offsets (n) likewise.
+ * *out_evals (may be NULL) = Q evaluations performed. */
+int cgpu_tables_build(cgpu_ctx* ctx, const uint32_t* primes, uint32_t n, int algorithm,
+                      uint8_t* out_bytes, uint32_t* out_offsets, uint64_t* out_evals);
+
+/* Uploads reference-format packed tables (e.g. from load_sieve or a tables
+ * .bin file) and makes them resident (replaces load_sieve for the device).
+ * Nonzero padding bits are a FormatError (sievetable.hpp:67-79). */
+int cgpu_tables_load(cgpu_ctx* ctx, const uint32_t* primes, uint32_t n, const uint8_t* bytes,
+                     uint64_t nbytes);
+
+/* Copies the resident packed tables back (total_bytes) -- byte-identical to
+ * serialize_tables (sievetable.hpp:229). */
+int cgpu_tables_download(cgpu_ctx* ctx, uint8_t* out_bytes, uint64_t cap);
+
+/* n primes resident (0 = none loaded); killable[k] = table k has a set bit. */
+int cgpu_tables_info(cgpu_ctx* ctx, uint32_t* n, uint8_t* killable);
+
+/* Stateless convenience: build on a temporary context of `device`. */
+int cgpu_build_tables(int device, const uint32_t* primes, uint32_t n, int algorithm,
+                      uint8_t* out_bytes, uint32_t* out_offsets, uint64_t* out_evals);
+
+/* ---- sieve ------------------------------------------------------------- */
+
+/* Sieves rows p in [p_lo, p_hi] against the resident tables (replaces the
+ * inner loops of scan(), engine.hpp:225-284). Rows are restricted to the
+ * block-cyclic shard (p/100) % shard_count == shard_index (shard_count 1 =
+ * all rows). REGION: the first row starts at q_start (0 = q_low(p_lo));
+ * TRIANGLE requires q_start == 0.
+ *
+ * Asynchronous: enqueues on the context stream and returns; results stay on
+ * the device until cgpu_sieve_results. The survivor buffer holds up to
+ * surv_cap pairs (the device counts beyond it; see CGPU_ERR_CAPACITY).
+ */
+int cgpu_sieve_launch(cgpu_ctx* ctx, uint64_t p_lo, uint64_t q_start, uint64_t p_hi, int mode,
+                      uint32_t shard_count, uint32_t shard_index, uint64_t surv_cap);
+
+/* Waits for the last launch and copies its results:
+ *   counts[2]      = {pairs_tested, survivors}
+ *   hist[n]        = first-killer counts by rank (ScanStats::kill_histogram)
+ *   block_rmax[nb] = per p/100 block max killing prime, 1 if none, for blocks
+ *                    p_lo/100 .. p_hi/100 (0 for blocks outside the shard)
+ *   surv_pq[2*k]   = survivors (p, q) ascending, k = min(survivors, cap)
+ * Any output pointer may be NULL. */
+int cgpu_sieve_results(cgpu_ctx* ctx, uint64_t* counts, uint64_t* hist, uint32_t* block_rmax,
+                       uint64_t block_cap, uint64_t* surv_pq, uint64_t surv_cap);
+
+/* Synchronous launch + results. */
+int cgpu_sieve(cgpu_ctx* ctx, uint64_t p_lo, uint64_t q_start, uint64_t p_hi, int mode,
+               uint32_t shard_count, uint32_t shard_index, uint64_t* counts, uint64_t* hist,
+               uint32_t* block_rmax, uint64_t block_cap, uint64_t* surv_pq, uint64_t surv_cap);
+
+/* Device time of the last launch's phases, from CUDA events on the context
+ * stream: ms[0] = plan kernel, ms[1] = sieve kernel, ms[2] = whole launch. */
+int cgpu_last_timings(cgpu_ctx* ctx, float* ms3);
+
+/* Number of kernels the last cgpu_sieve_launch / cgpu_tables_* enqueued. */
+int cgpu_last_launch_count(cgpu_ctx* ctx, uint32_t* n);
+
+/* ---- classify (K3) ------------------------------------------------------- */
+
+/* First-killer rank for explicit pairs (verify_pair's sieve part,
+ * engine.hpp:72-78): out_rank[i] = rank of the smallest-rank prime whose table
+ * rejects (p_i, q_i), or -1 if no table does. pq = n pairs of u64 (p, q). */
+int cgpu_classify(cgpu_ctx* ctx, const uint64_t* pq, uint64_t n, int32_t* out_rank);
+
+/* ---- region arithmetic (host) -------------------------------------------- */
+
+/* q_bounds (region.hpp:49-63). */
+int cgpu_q_bounds(uint64_t p, uint64_t* q_low, uint64_t* q_high);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CUBOID_GPU_H */

@@ -1,0 +1,86 @@
+"""ctypes binding of libcuboid_gpu.so (include/cuboid_gpu.h).
+
+The product path has no CPU fallback: if the library is missing, or no CUDA
+device is visible, every entry point raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libcuboid_gpu.so")
+
+# status codes (cuboid_gpu.h)
+OK = 0
+P_BELOW_152, P_ABOVE_LIMIT, Q_BELOW_LOW, Q_ABOVE_HIGH, NOT_LOADED = 2, 3, 4, 5, 6
+ERR_CUDA, ERR_INVALID, ERR_OVERFLOW, ERR_FORMAT, ERR_RANGE, ERR_CAPACITY, ERR_NO_DEVICE = (
+    -1, -2, -3, -4, -5, -6, -7)
+REGION, TRIANGLE = 0, 1
+BUILD_PRODUCTION, BUILD_EXHAUSTIVE = 0, 1
+
+_u64p = C.POINTER(C.c_uint64)
+_u32p = C.POINTER(C.c_uint32)
+
+# name -> (restype, argtypes); every symbol include/cuboid_gpu.h declares
+SIGNATURES = {
+    "cgpu_last_error": (C.c_char_p, []),
+    "cgpu_version": (C.c_char_p, []),
+    "cgpu_create": (C.c_int, [C.c_int, C.c_void_p, C.POINTER(C.c_void_p)]),
+    "cgpu_destroy": (C.c_int, [C.c_void_p]),
+    "cgpu_set_stream": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "cgpu_synchronize": (C.c_int, [C.c_void_p]),
+    "cgpu_table_layout": (C.c_int, [C.c_void_p, C.c_uint32, C.c_void_p, _u64p]),
+    "cgpu_tables_build": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint32, C.c_int, C.c_void_p,
+                                    C.c_void_p, _u64p]),
+    "cgpu_tables_load": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint32, C.c_void_p, C.c_uint64]),
+    "cgpu_tables_download": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64]),
+    "cgpu_tables_info": (C.c_int, [C.c_void_p, _u32p, C.c_void_p]),
+    "cgpu_build_tables": (C.c_int, [C.c_int, C.c_void_p, C.c_uint32, C.c_int, C.c_void_p,
+                                    C.c_void_p, _u64p]),
+    "cgpu_sieve_launch": (C.c_int, [C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint64, C.c_int,
+                                    C.c_uint32, C.c_uint32, C.c_uint64]),
+    "cgpu_sieve_results": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64,
+                                     C.c_void_p, C.c_uint64]),
+    "cgpu_sieve": (C.c_int, [C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint64, C.c_int, C.c_uint32,
+                             C.c_uint32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64,
+                             C.c_void_p, C.c_uint64]),
+    "cgpu_last_timings": (C.c_int, [C.c_void_p, C.POINTER(C.c_float)]),
+    "cgpu_last_launch_count": (C.c_int, [C.c_void_p, _u32p]),
+    "cgpu_classify": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p]),
+    "cgpu_q_bounds": (C.c_int, [C.c_uint64, _u64p, _u64p]),
+}
+
+_lib = None
+
+
+class CudaSieveError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"cuboid_gpu status {code}: {msg}")
+        self.code = code
+
+
+def lib():
+    """Load libcuboid_gpu.so; raises if it is missing (no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} not built: run __graft_entry__.build() "
+                              "(make -C paper_1601_00636_b200)")
+        L = C.CDLL(LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = L
+    return _lib
+
+
+def last_error() -> str:
+    return lib().cgpu_last_error().decode()
+
+
+def check(rc):
+    if rc != OK:
+        raise CudaSieveError(rc, last_error())
+    return rc

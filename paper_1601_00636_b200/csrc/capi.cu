@@ -1,0 +1,656 @@
+// C ABI (include/cuboid_gpu.h): device context, resident table sets, sieve
+// launches and result collection. No exceptions cross the boundary; status
+// codes mirror the reference's exceptions (see the header).
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/cuboid_gpu.h"
+#include "common.cuh"
+#include "kernels.cuh"
+
+using namespace cgpu;
+
+namespace {
+
+thread_local std::string g_err;
+
+int set_err(int code, const std::string& msg)
+{
+	g_err = msg;
+	return code;
+}
+
+#define CK(call)                                                                            \
+	do {                                                                                    \
+		const cudaError_t e_ = (call);                                                      \
+		if (e_ != cudaSuccess)                                                              \
+			return set_err(CGPU_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+	} while (0)
+
+template <class T>
+struct DevBuf {
+	T* p = nullptr;
+	size_t n = 0;
+	~DevBuf() { release(); }
+	void release()
+	{
+		if (p) cudaFree(p);
+		p = nullptr;
+		n = 0;
+	}
+	cudaError_t ensure(size_t want)
+	{
+		if (want <= n && p) return cudaSuccess;
+		release();
+		const size_t bytes = sizeof(T) * (want ? want : 1);
+		cudaError_t e = cudaMalloc(&p, bytes);
+		if (e == cudaSuccess) n = want ? want : 1;
+		return e;
+	}
+};
+
+bool is_prime_u32(uint32_t n)  // primes.hpp:14-21
+{
+	if (n < 2) return false;
+	if (n % 2 == 0) return n == 2;
+	for (uint32_t d = 3; d * d <= n; d += 2)
+		if (n % d == 0) return false;
+	return true;
+}
+
+uint64_t table_bytes(uint32_t r) { return (static_cast<uint64_t>(r) * r + 7) / 8; }
+
+// SieveSet::build validation order (sievetable.hpp:159-176, 83-87).
+int layout(const uint32_t* primes, uint32_t n, uint32_t* offsets, uint64_t* total)
+{
+	if (n && !primes) return set_err(CGPU_ERR_INVALID, "null prime list");
+	uint64_t off = 0;
+	uint32_t prev = 0;
+	for (uint32_t k = 0; k < n; ++k) {
+		const uint32_t r = primes[k];
+		if (r <= prev)
+			return set_err(CGPU_ERR_INVALID, "SieveSet::build: primes must be strictly increasing");
+		prev = r;
+		if (r < 2 || r >= kModulusLimit || !is_prime_u32(r))
+			return set_err(CGPU_ERR_INVALID, "bit table modulus must be a prime below 9697");
+		if (off + table_bytes(r) > UINT32_MAX)
+			return set_err(CGPU_ERR_OVERFLOW,
+			               "SieveSet::build: table set exceeds 32-bit offset space");
+		if (offsets) offsets[k] = static_cast<uint32_t>(off);
+		off += table_bytes(r);
+	}
+	if (total) *total = off;
+	return CGPU_OK;
+}
+
+uint64_t q_lower_cubic(uint64_t p)  // region.hpp:25-39
+{
+	uint64_t lo = 1, hi = 1;
+	auto ge = [p](uint64_t q) { return 9 * (static_cast<unsigned __int128>(q) * q * q) >= p; };
+	while (!ge(hi)) hi *= 2;
+	while (lo < hi) {
+		const uint64_t mid = lo + (hi - lo) / 2;
+		if (ge(mid)) hi = mid; else lo = mid + 1;
+	}
+	return lo;
+}
+
+void q_bounds(uint64_t p, uint64_t* lo, uint64_t* hi)  // region.hpp:49-63
+{
+	*hi = 59 * p;
+	if (p < kRegionCrossover) {
+		const uint64_t c = (p + 58) / 59;
+		*lo = c < 1 ? 1 : c;
+	} else {
+		*lo = q_lower_cubic(p);
+	}
+}
+
+constexpr uint32_t kMaxSlots = 1u << 20;  // row slots per plan/sieve launch (multiple of 100 below)
+constexpr uint32_t kBlocksPerLaunch = kMaxSlots / 100;
+
+}  // namespace
+
+struct cgpu_ctx {
+	int device = 0;
+	cudaStream_t stream = nullptr;
+	bool own_stream = false;
+	int sms = 0;
+
+	// resident set
+	bool loaded = false;
+	std::vector<uint32_t> primes, offsets, ext_base;
+	std::vector<uint8_t> killable;
+	uint64_t total_bytes = 0, ext_words = 0;
+	DevBuf<uint8_t> packed;
+	DevBuf<uint32_t> ext, d_primes, d_offsets, killflags;
+	DevBuf<PrimeJob> jobs_rank;
+
+	// probe list
+	uint32_t np = 0, nreg = 0;
+	std::vector<uint32_t> probe_rank, probe_r;
+	DevBuf<uint4> probes;
+	uint32_t reg_r[kMaxReg] = {}, reg_m[kMaxReg] = {}, reg_base[kMaxReg] = {}, reg_delta[kMaxReg] = {};
+	int grid[kMaxReg + 1] = {};
+
+	DevBuf<uint2> fprimes;
+	uint32_t n_fprimes = 0;
+
+	// sieve buffers
+	DevBuf<unsigned long long> hist_probe, counters, surv, prefix;
+	DevBuf<uint32_t> block_rmax;
+	bool launched = false;
+	uint64_t last_nblocks = 0, last_surv_cap = 0;
+	cudaEvent_t ev[3] = {};
+	float timings[3] = {};
+	uint32_t launches = 0;
+
+	// scratch
+	DevBuf<uint8_t> row1;
+	DevBuf<uint32_t> inv;
+	DevBuf<unsigned long long> evals;
+	DevBuf<PrimeJob> jobs_build;
+	DevBuf<uint64_t> pq;
+	DevBuf<int32_t> ranks;
+};
+
+extern "C" {
+
+const char* cgpu_last_error(void) { return g_err.c_str(); }
+
+const char* cgpu_version(void) { return "cuboid-gpu 0.1 sm_100a"; }
+
+int cgpu_q_bounds(uint64_t p, uint64_t* q_low, uint64_t* q_high)
+{
+	if (p == 0) return set_err(CGPU_ERR_INVALID, "q_bounds: p must be positive");
+	if (p > UINT64_MAX / 59) return set_err(CGPU_ERR_OVERFLOW, "q_bounds: 59p exceeds 64 bits");
+	q_bounds(p, q_low, q_high);
+	return CGPU_OK;
+}
+
+int cgpu_table_layout(const uint32_t* primes, uint32_t n, uint32_t* offsets, uint64_t* total_bytes)
+{
+	return layout(primes, n, offsets, total_bytes);
+}
+
+int cgpu_create(int device, void* stream, cgpu_ctx** out)
+{
+	if (!out) return set_err(CGPU_ERR_INVALID, "null out");
+	*out = nullptr;
+	int count = 0;
+	if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0)
+		return set_err(CGPU_ERR_NO_DEVICE, "no CUDA device visible: cuboid_gpu has no CPU fallback");
+	if (device < 0 || device >= count) return set_err(CGPU_ERR_INVALID, "device index out of range");
+	CK(cudaSetDevice(device));
+	auto* c = new cgpu_ctx;
+	c->device = device;
+	if (stream) {
+		c->stream = static_cast<cudaStream_t>(stream);
+	} else {
+		if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) {
+			delete c;
+			return set_err(CGPU_ERR_CUDA, "cudaStreamCreate failed");
+		}
+		c->own_stream = true;
+	}
+	cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device);
+	for (auto& e : c->ev) cudaEventCreate(&e);
+	// trial-division primes below 2^16 (covers sqrt of any p < 2^32)
+	std::vector<uint2> fp;
+	{
+		std::vector<uint8_t> comp(65536, 0);
+		for (uint32_t i = 2; i < 65536; ++i) {
+			if (comp[i]) continue;
+			fp.push_back(make_uint2(i, barrett_m(i)));
+			for (uint32_t j = i * i; j < 65536; j += i) comp[j] = 1;
+		}
+	}
+	c->n_fprimes = static_cast<uint32_t>(fp.size());
+	if (c->fprimes.ensure(fp.size()) != cudaSuccess ||
+	    cudaMemcpy(c->fprimes.p, fp.data(), sizeof(uint2) * fp.size(), cudaMemcpyHostToDevice) !=
+	        cudaSuccess) {
+		delete c;
+		return set_err(CGPU_ERR_CUDA, "device allocation failed");
+	}
+	*out = c;
+	return CGPU_OK;
+}
+
+int cgpu_destroy(cgpu_ctx* c)
+{
+	if (!c) return CGPU_OK;
+	cudaSetDevice(c->device);
+	cudaStreamSynchronize(c->stream);
+	for (auto& e : c->ev)
+		if (e) cudaEventDestroy(e);
+	if (c->own_stream) cudaStreamDestroy(c->stream);
+	delete c;
+	return CGPU_OK;
+}
+
+int cgpu_set_stream(cgpu_ctx* c, void* stream)
+{
+	if (!c) return set_err(CGPU_ERR_INVALID, "null ctx");
+	CK(cudaSetDevice(c->device));
+	CK(cudaStreamSynchronize(c->stream));
+	if (c->own_stream) cudaStreamDestroy(c->stream);
+	c->own_stream = false;
+	c->stream = static_cast<cudaStream_t>(stream);
+	if (!stream) {
+		CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+		c->own_stream = true;
+	}
+	return CGPU_OK;
+}
+
+int cgpu_synchronize(cgpu_ctx* c)
+{
+	if (!c) return set_err(CGPU_ERR_INVALID, "null ctx");
+	CK(cudaSetDevice(c->device));
+	CK(cudaStreamSynchronize(c->stream));
+	return CGPU_OK;
+}
+
+}  // extern "C"
+
+namespace {
+
+std::vector<PrimeJob> make_jobs(const std::vector<uint32_t>& primes,
+                                const std::vector<uint32_t>& offsets, std::vector<uint32_t>& ext_base,
+                                uint64_t& ext_words)
+{
+	std::vector<PrimeJob> jobs(primes.size());
+	ext_base.resize(primes.size());
+	uint64_t ext = 0, aux = 0;
+	for (size_t k = 0; k < primes.size(); ++k) {
+		const uint32_t r = primes[k];
+		jobs[k] = PrimeJob{r, barrett_m(r), offsets[k], static_cast<uint32_t>(ext),
+		                   static_cast<uint32_t>(aux), 0};
+		ext_base[k] = static_cast<uint32_t>(ext);
+		ext += static_cast<uint64_t>(r) * ext_row_words(r);
+		aux += r;
+	}
+	ext_words = ext;
+	return jobs;
+}
+
+// After the packed bytes are resident: derive ext rows + killable flags, then
+// build the probe list (killable tables in rank order).
+int finalize_set(cgpu_ctx* c)
+{
+	const uint32_t n = static_cast<uint32_t>(c->primes.size());
+	std::vector<PrimeJob> jobs = make_jobs(c->primes, c->offsets, c->ext_base, c->ext_words);
+	if (c->ext_words >= (1ull << 32))
+		return set_err(CGPU_ERR_OVERFLOW, "row-extended layout exceeds 2^32 words");
+	CK(c->jobs_rank.ensure(n));
+	CK(c->ext.ensure(c->ext_words));
+	CK(c->killflags.ensure(n));
+	CK(c->d_primes.ensure(n));
+	CK(c->d_offsets.ensure(n));
+	if (n) {
+		CK(cudaMemcpyAsync(c->jobs_rank.p, jobs.data(), sizeof(PrimeJob) * n, cudaMemcpyHostToDevice,
+		                   c->stream));
+		CK(cudaMemcpyAsync(c->d_primes.p, c->primes.data(), 4ull * n, cudaMemcpyHostToDevice, c->stream));
+		CK(cudaMemcpyAsync(c->d_offsets.p, c->offsets.data(), 4ull * n, cudaMemcpyHostToDevice,
+		                   c->stream));
+		CK(cudaMemsetAsync(c->killflags.p, 0, 4ull * n, c->stream));
+		uint64_t max_words = 0;
+		for (auto r : c->primes) max_words = std::max<uint64_t>(max_words, uint64_t(r) * ext_row_words(r));
+		CK(launch_derive(c->jobs_rank.p, n, max_words, c->packed.p, c->ext.p, c->killflags.p, c->stream));
+		++c->launches;
+	}
+	std::vector<uint32_t> kf(n);
+	if (n) CK(cudaMemcpyAsync(kf.data(), c->killflags.p, 4ull * n, cudaMemcpyDeviceToHost, c->stream));
+	CK(cudaStreamSynchronize(c->stream));
+	c->killable.assign(n, 0);
+	c->probe_rank.clear();
+	c->probe_r.clear();
+	std::vector<uint4> pr;
+	for (uint32_t k = 0; k < n; ++k) {
+		c->killable[k] = kf[k] ? 1 : 0;
+		if (!kf[k]) continue;  // an all-zero table never kills: skipping it is exact
+		const uint32_t r = c->primes[k];
+		c->probe_rank.push_back(k);
+		c->probe_r.push_back(r);
+		pr.push_back(make_uint4(r, barrett_m(r), c->ext_base[k], ext_row_words(r)));
+	}
+	c->np = static_cast<uint32_t>(pr.size());
+	c->nreg = 0;
+	while (c->nreg < c->np && c->nreg < static_cast<uint32_t>(kMaxReg) && c->probe_r[c->nreg] <= 31) {
+		const uint32_t j = c->nreg, r = c->probe_r[j];
+		c->reg_r[j] = r;
+		c->reg_m[j] = barrett_m(r);
+		c->reg_base[j] = pr[j].z;
+		c->reg_delta[j] = (32u * 32u) % r;
+		++c->nreg;
+	}
+	CK(c->probes.ensure(c->np));
+	if (c->np)
+		CK(cudaMemcpyAsync(c->probes.p, pr.data(), sizeof(uint4) * c->np, cudaMemcpyHostToDevice,
+		                   c->stream));
+	CK(c->hist_probe.ensure(c->np));
+	const size_t smem = sieve_smem_bytes(c->np);
+	if (smem > 220 * 1024)
+		return set_err(CGPU_ERR_INVALID, "too many probe primes for the sieve's shared memory");
+	c->grid[c->nreg] = sieve_grid(c->device, static_cast<int>(c->nreg), smem);
+	CK(cudaGetLastError());
+	CK(cudaStreamSynchronize(c->stream));
+	c->loaded = true;
+	c->launched = false;
+	return CGPU_OK;
+}
+
+int begin_set(cgpu_ctx* c, const uint32_t* primes, uint32_t n)
+{
+	std::vector<uint32_t> offs(n);
+	uint64_t total = 0;
+	if (int rc = layout(primes, n, offs.data(), &total)) return rc;
+	c->loaded = false;
+	c->primes.assign(primes, primes + n);
+	c->offsets = offs;
+	c->total_bytes = total;
+	CK(c->packed.ensure(total));
+	return CGPU_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int cgpu_tables_build(cgpu_ctx* c, const uint32_t* primes, uint32_t n, int algorithm,
+                      uint8_t* out_bytes, uint32_t* out_offsets, uint64_t* out_evals)
+{
+	if (!c) return set_err(CGPU_ERR_INVALID, "null ctx");
+	if (algorithm != CGPU_BUILD_PRODUCTION && algorithm != CGPU_BUILD_EXHAUSTIVE)
+		return set_err(CGPU_ERR_INVALID, "unknown build algorithm");
+	CK(cudaSetDevice(c->device));
+	if (int rc = begin_set(c, primes, n)) return rc;
+	c->launches = 0;
+	uint64_t evals = 0;
+	if (n) {
+		std::vector<uint32_t> eb;
+		uint64_t ew = 0;
+		std::vector<PrimeJob> jobs = make_jobs(c->primes, c->offsets, eb, ew);
+		std::vector<PrimeJob> byr = jobs;
+		std::stable_sort(byr.begin(), byr.end(), [](const PrimeJob& x, const PrimeJob& y) { return x.r > y.r; });
+		CK(c->jobs_build.ensure(n));
+		CK(cudaMemcpyAsync(c->jobs_build.p, byr.data(), sizeof(PrimeJob) * n, cudaMemcpyHostToDevice,
+		                   c->stream));
+		CK(cudaMemsetAsync(c->packed.p, 0, c->total_bytes, c->stream));
+		const uint32_t rmax = byr.front().r;
+		if (algorithm == CGPU_BUILD_EXHAUSTIVE) {
+			CK(launch_cube(c->jobs_build.p, n, rmax * rmax, c->packed.p, c->stream));
+			c->launches += 1;
+			for (auto r : c->primes) evals += static_cast<uint64_t>(r) * r * r;
+		} else {
+			uint64_t aux = 0;
+			for (auto r : c->primes) aux += r;
+			CK(c->row1.ensure(aux));
+			CK(c->inv.ensure(aux));
+			CK(c->evals.ensure(1));
+			CK(cudaMemsetAsync(c->evals.p, 0, 8, c->stream));
+			CK(launch_row1(c->jobs_build.p, n, rmax, c->row1.p, c->inv.p, c->evals.p, c->stream));
+			CK(launch_permute(c->jobs_build.p, n, rmax * rmax, c->row1.p, c->inv.p, c->packed.p,
+			                  c->stream));
+			c->launches += 2;
+			unsigned long long ev = 0;
+			CK(cudaMemcpyAsync(&ev, c->evals.p, 8, cudaMemcpyDeviceToHost, c->stream));
+			CK(cudaStreamSynchronize(c->stream));
+			evals = ev;
+		}
+	}
+	if (int rc = finalize_set(c)) return rc;
+	if (out_bytes && c->total_bytes) {
+		CK(cudaMemcpyAsync(out_bytes, c->packed.p, c->total_bytes, cudaMemcpyDeviceToHost, c->stream));
+		CK(cudaStreamSynchronize(c->stream));
+	}
+	if (out_offsets && n) std::memcpy(out_offsets, c->offsets.data(), 4ull * n);
+	if (out_evals) *out_evals = evals;
+	return CGPU_OK;
+}
+
+int cgpu_tables_load(cgpu_ctx* c, const uint32_t* primes, uint32_t n, const uint8_t* bytes,
+                     uint64_t nbytes)
+{
+	if (!c) return set_err(CGPU_ERR_INVALID, "null ctx");
+	CK(cudaSetDevice(c->device));
+	uint64_t total = 0;
+	if (int rc = layout(primes, n, nullptr, &total)) return rc == CGPU_ERR_INVALID ? set_err(CGPU_ERR_FORMAT, g_err) : rc;
+	if (total != nbytes) return set_err(CGPU_ERR_FORMAT, "load_sieve: tables stream length does not match index");
+	if (int rc = begin_set(c, primes, n)) return rc;
+	c->launches = 0;
+	if (n) {
+		if (!bytes) return set_err(CGPU_ERR_INVALID, "null table bytes");
+		CK(cudaMemcpyAsync(c->packed.p, bytes, total, cudaMemcpyHostToDevice, c->stream));
+		std::vector<uint32_t> eb;
+		uint64_t ew = 0;
+		std::vector<PrimeJob> jobs = make_jobs(c->primes, c->offsets, eb, ew);
+		CK(c->jobs_rank.ensure(n));
+		CK(cudaMemcpyAsync(c->jobs_rank.p, jobs.data(), sizeof(PrimeJob) * n, cudaMemcpyHostToDevice,
+		                   c->stream));
+		CK(c->evals.ensure(1));
+		CK(cudaMemsetAsync(c->evals.p, 0, 8, c->stream));
+		CK(launch_check_padding(c->jobs_rank.p, n, c->packed.p,
+		                        reinterpret_cast<uint32_t*>(c->evals.p), c->stream));
+		++c->launches;
+		uint32_t bad = 0;
+		CK(cudaMemcpyAsync(&bad, c->evals.p, 4, cudaMemcpyDeviceToHost, c->stream));
+		CK(cudaStreamSynchronize(c->stream));
+		if (bad) return set_err(CGPU_ERR_FORMAT, "unpack_bits: nonzero padding bits");
+	}
+	return finalize_set(c);
+}
+
+int cgpu_tables_download(cgpu_ctx* c, uint8_t* out, uint64_t cap)
+{
+	if (!c) return set_err(CGPU_ERR_INVALID, "null ctx");
+	if (!c->loaded) return set_err(CGPU_NOT_LOADED, "tables not loaded");
+	if (cap < c->total_bytes) return set_err(CGPU_ERR_CAPACITY, "output buffer too small");
+	CK(cudaSetDevice(c->device));
+	if (c->total_bytes) {
+		CK(cudaMemcpyAsync(out, c->packed.p, c->total_bytes, cudaMemcpyDeviceToHost, c->stream));
+		CK(cudaStreamSynchronize(c->stream));
+	}
+	return CGPU_OK;
+}
+
+int cgpu_tables_info(cgpu_ctx* c, uint32_t* n, uint8_t* killable)
+{
+	if (!c) return set_err(CGPU_ERR_INVALID, "null ctx");
+	const uint32_t k = c->loaded ? static_cast<uint32_t>(c->primes.size()) : 0;
+	if (n) *n = k;
+	if (killable && k) std::memcpy(killable, c->killable.data(), k);
+	return CGPU_OK;
+}
+
+int cgpu_build_tables(int device, const uint32_t* primes, uint32_t n, int algorithm,
+                      uint8_t* out_bytes, uint32_t* out_offsets, uint64_t* out_evals)
+{
+	cgpu_ctx* c = nullptr;
+	if (int rc = cgpu_create(device, nullptr, &c)) return rc;
+	const int rc = cgpu_tables_build(c, primes, n, algorithm, out_bytes, out_offsets, out_evals);
+	const std::string keep = g_err;
+	cgpu_destroy(c);
+	g_err = keep;
+	return rc;
+}
+
+int cgpu_sieve_launch(cgpu_ctx* c, uint64_t p_lo, uint64_t q_start, uint64_t p_hi, int mode,
+                      uint32_t G, uint32_t g, uint64_t surv_cap)
+{
+	if (!c) return set_err(CGPU_ERR_INVALID, "null ctx");
+	if (!c->loaded || c->primes.empty()) return set_err(CGPU_NOT_LOADED, "tables not loaded");
+	if (mode != CGPU_REGION && mode != CGPU_TRIANGLE) return set_err(CGPU_ERR_INVALID, "unknown mode");
+	if (G == 0 || g >= G) return set_err(CGPU_ERR_INVALID, "bad shard (count, index)");
+	if (p_lo == 0) return set_err(CGPU_P_ABOVE_LIMIT, "p must be positive");
+	if (mode == CGPU_REGION) {
+		if (p_hi > kPLimit32 || p_lo > kPLimit32)
+			return set_err(CGPU_P_ABOVE_LIMIT, "p above the 32-bit region limit");
+		if (q_start) {
+			uint64_t lo, hi;
+			q_bounds(p_lo, &lo, &hi);
+			if (q_start < lo) return set_err(CGPU_Q_BELOW_LOW, "q below q_low");
+			if (q_start > hi) return set_err(CGPU_Q_ABOVE_HIGH, "q above q_high");
+		}
+	} else {
+		if (q_start) return set_err(CGPU_ERR_INVALID, "TRIANGLE mode sieves whole rows (q_start must be 0)");
+		if (p_hi > 0xffffffffull) return set_err(CGPU_P_ABOVE_LIMIT, "p above 2^32");
+	}
+	CK(cudaSetDevice(c->device));
+	c->launched = false;
+	c->launches = 0;
+	const bool empty = p_hi < p_lo;
+	const uint64_t blk_lo = p_lo / 100;
+	const uint64_t nblocks = empty ? 0 : p_hi / 100 - blk_lo + 1;
+	CK(c->hist_probe.ensure(c->np));
+	CK(c->counters.ensure(2));
+	CK(c->block_rmax.ensure(nblocks));
+	CK(c->surv.ensure(surv_cap));
+	CK(cudaMemsetAsync(c->hist_probe.p, 0, 8ull * c->np, c->stream));
+	CK(cudaMemsetAsync(c->counters.p, 0, 16, c->stream));
+	CK(launch_init_blocks(c->block_rmax.p, nblocks, blk_lo, G, g, c->stream));
+	++c->launches;
+	CK(cudaEventRecord(c->ev[0], c->stream));
+	CK(cudaEventRecord(c->ev[1], c->stream));
+
+	SieveArgs a{};
+	a.ext = c->ext.p;
+	a.probes = c->probes.p;
+	a.np = c->np;
+	a.nreg = c->nreg;
+	for (int j = 0; j < kMaxReg; ++j) {
+		a.reg_r[j] = c->reg_r[j];
+		a.reg_m[j] = c->reg_m[j];
+		a.reg_base[j] = c->reg_base[j];
+		a.reg_delta[j] = c->reg_delta[j];
+	}
+	a.fprimes = c->fprimes.p;
+	a.n_fprimes = c->n_fprimes;
+	a.p_lo = p_lo;
+	a.p_hi = p_hi;
+	a.q_start = q_start;
+	a.mode = mode;
+	a.G = G;
+	a.hist_probe = c->hist_probe.p;
+	a.counters = c->counters.p;
+	a.block_rmax = c->block_rmax.p;
+	a.blk_lo = blk_lo;
+	a.surv = c->surv.p;
+	a.surv_cap = surv_cap;
+
+	if (!empty && c->np) {
+		// owned blocks: b in [blk_lo, blk_hi] with b % G == g
+		const uint64_t blk_hi = p_hi / 100;
+		const uint64_t first = blk_lo + ((g + G - blk_lo % G) % G);
+		const uint64_t owned = first <= blk_hi ? (blk_hi - first) / G + 1 : 0;
+		CK(c->prefix.ensure(static_cast<size_t>(std::min<uint64_t>(owned, kBlocksPerLaunch)) * 100 + 1));
+		bool first_chunk = true;
+		for (uint64_t ob = 0; ob < owned; ob += kBlocksPerLaunch) {
+			const uint64_t nb = std::min<uint64_t>(kBlocksPerLaunch, owned - ob);
+			a.blk0 = first + ob * G;
+			a.n_slots = static_cast<uint32_t>(nb * 100);
+			a.prefix = c->prefix.p;
+			CK(launch_plan(a, c->prefix.p, c->stream));
+			if (first_chunk) CK(cudaEventRecord(c->ev[1], c->stream));
+			first_chunk = false;
+			CK(launch_sieve(a, c->grid[c->nreg], c->stream));
+			c->launches += 2;
+		}
+	}
+	CK(cudaEventRecord(c->ev[2], c->stream));
+	c->last_nblocks = nblocks;
+	c->last_surv_cap = surv_cap;
+	c->launched = true;
+	return CGPU_OK;
+}
+
+int cgpu_sieve_results(cgpu_ctx* c, uint64_t* counts, uint64_t* hist, uint32_t* block_rmax,
+                       uint64_t block_cap, uint64_t* surv_pq, uint64_t surv_cap)
+{
+	if (!c) return set_err(CGPU_ERR_INVALID, "null ctx");
+	if (!c->launched) return set_err(CGPU_ERR_INVALID, "no sieve launched");
+	CK(cudaSetDevice(c->device));
+	unsigned long long cnt[2] = {0, 0};
+	std::vector<unsigned long long> hp(c->np);
+	CK(cudaMemcpyAsync(cnt, c->counters.p, 16, cudaMemcpyDeviceToHost, c->stream));
+	if (c->np)
+		CK(cudaMemcpyAsync(hp.data(), c->hist_probe.p, 8ull * c->np, cudaMemcpyDeviceToHost, c->stream));
+	if (block_rmax && c->last_nblocks) {
+		if (block_cap < c->last_nblocks) return set_err(CGPU_ERR_CAPACITY, "block_rmax buffer too small");
+		CK(cudaMemcpyAsync(block_rmax, c->block_rmax.p, 4ull * c->last_nblocks, cudaMemcpyDeviceToHost,
+		                   c->stream));
+	}
+	CK(cudaStreamSynchronize(c->stream));
+	float ms = 0;
+	if (cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]) == cudaSuccess) c->timings[0] = ms;
+	if (cudaEventElapsedTime(&ms, c->ev[1], c->ev[2]) == cudaSuccess) c->timings[1] = ms;
+	if (cudaEventElapsedTime(&ms, c->ev[0], c->ev[2]) == cudaSuccess) c->timings[2] = ms;
+	if (counts) {
+		counts[0] = cnt[0];
+		counts[1] = cnt[1];
+	}
+	if (hist) {
+		std::fill(hist, hist + c->primes.size(), 0ull);
+		for (uint32_t j = 0; j < c->np; ++j) hist[c->probe_rank[j]] = hp[j];
+	}
+	int rc = CGPU_OK;
+	if (surv_pq && cnt[1]) {
+		const uint64_t stored = std::min<uint64_t>(cnt[1], c->last_surv_cap);
+		std::vector<unsigned long long> keys(stored);
+		CK(cudaMemcpyAsync(keys.data(), c->surv.p, 8 * stored, cudaMemcpyDeviceToHost, c->stream));
+		CK(cudaStreamSynchronize(c->stream));
+		std::sort(keys.begin(), keys.end());
+		const uint64_t k = std::min<uint64_t>(stored, surv_cap);
+		for (uint64_t i = 0; i < k; ++i) {
+			surv_pq[2 * i] = keys[i] >> 32;
+			surv_pq[2 * i + 1] = keys[i] & 0xffffffffull;
+		}
+		if (cnt[1] > k) rc = set_err(CGPU_ERR_CAPACITY, "survivor buffer too small");
+	}
+	return rc;
+}
+
+int cgpu_sieve(cgpu_ctx* c, uint64_t p_lo, uint64_t q_start, uint64_t p_hi, int mode, uint32_t G,
+               uint32_t g, uint64_t* counts, uint64_t* hist, uint32_t* block_rmax, uint64_t block_cap,
+               uint64_t* surv_pq, uint64_t surv_cap)
+{
+	if (int rc = cgpu_sieve_launch(c, p_lo, q_start, p_hi, mode, G, g, surv_pq ? surv_cap : 0)) return rc;
+	return cgpu_sieve_results(c, counts, hist, block_rmax, block_cap, surv_pq, surv_cap);
+}
+
+int cgpu_last_timings(cgpu_ctx* c, float* ms3)
+{
+	if (!c || !ms3) return set_err(CGPU_ERR_INVALID, "null argument");
+	std::memcpy(ms3, c->timings, sizeof c->timings);
+	return CGPU_OK;
+}
+
+int cgpu_last_launch_count(cgpu_ctx* c, uint32_t* n)
+{
+	if (!c || !n) return set_err(CGPU_ERR_INVALID, "null argument");
+	*n = c->launches;
+	return CGPU_OK;
+}
+
+int cgpu_classify(cgpu_ctx* c, const uint64_t* pq, uint64_t n, int32_t* out_rank)
+{
+	if (!c) return set_err(CGPU_ERR_INVALID, "null ctx");
+	if (!c->loaded || c->primes.empty()) return set_err(CGPU_NOT_LOADED, "tables not loaded");
+	if (!n) return CGPU_OK;
+	CK(cudaSetDevice(c->device));
+	CK(c->pq.ensure(2 * n));
+	CK(c->ranks.ensure(n));
+	CK(cudaMemcpyAsync(c->pq.p, pq, 16 * n, cudaMemcpyHostToDevice, c->stream));
+	CK(launch_classify(c->pq.p, n, c->packed.p, c->d_primes.p, c->d_offsets.p,
+	                   static_cast<uint32_t>(c->primes.size()), c->ranks.p, c->stream));
+	c->launches = 1;
+	CK(cudaMemcpyAsync(out_rank, c->ranks.p, 4 * n, cudaMemcpyDeviceToHost, c->stream));
+	CK(cudaStreamSynchronize(c->stream));
+	return CGPU_OK;
+}
+
+}  // extern "C"

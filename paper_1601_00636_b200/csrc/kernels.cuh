@@ -1,0 +1,94 @@
+// Host-side launchers for the device kernels (tables.cu, sieve.cu).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace cgpu {
+
+// ---- K1: residue tables ------------------------------------------------------
+
+// One prime of a set being built/derived on the device.
+struct PrimeJob {
+	uint32_t r;         // prime
+	uint32_t m;         // barrett_m(r)
+	uint32_t byte_off;  // offset of its packed table in the set
+	uint32_t ext_base;  // word offset of its ext rows
+	uint32_t aux_off;   // offset into per-prime scratch (row1 / inverses), sum of r
+	uint32_t pad;
+};
+
+// Exhaustive cube: all (a,b,t) in Z_r^3, no early exit. `jobs` sorted by
+// descending r (blockIdx.y = job); max_rr = largest r^2.
+cudaError_t launch_cube(const PrimeJob* d_jobs, uint32_t njobs, uint32_t max_rr,
+                        uint8_t* d_packed, cudaStream_t s);
+
+// Production: row 1 (t <= r/2, early exit) + modular inverses, then the
+// permuted, packed r x r table.
+cudaError_t launch_row1(const PrimeJob* d_jobs, uint32_t njobs, uint32_t max_r,
+                        uint8_t* d_row1, uint32_t* d_inv, unsigned long long* d_evals,
+                        cudaStream_t s);
+cudaError_t launch_permute(const PrimeJob* d_jobs, uint32_t njobs, uint32_t max_rr,
+                           const uint8_t* d_row1, const uint32_t* d_inv, uint8_t* d_packed,
+                           cudaStream_t s);
+
+// Packed reference bytes -> row-extended words + killable flags; jobs in rank
+// order (killable index = blockIdx.y). max_words = largest r * ext_row_words(r).
+cudaError_t launch_derive(const PrimeJob* d_jobs, uint32_t njobs, uint64_t max_words,
+                          const uint8_t* d_packed, uint32_t* d_ext, uint32_t* d_killable,
+                          cudaStream_t s);
+
+// Padding-bit check for uploaded tables (FormatError on nonzero padding).
+cudaError_t launch_check_padding(const PrimeJob* d_jobs, uint32_t njobs, const uint8_t* d_packed,
+                                 uint32_t* d_bad, cudaStream_t s);
+
+constexpr uint32_t kCubeThreads = 256;
+constexpr uint32_t kPermThreads = 256;
+constexpr uint32_t kRow1Threads = 128;
+constexpr uint32_t kDeriveThreads = 256;
+
+// ---- K2: sieve ---------------------------------------------------------------
+
+constexpr int kSieveThreads = 256;
+constexpr int kSieveWarps = kSieveThreads / 32;
+constexpr int kMaxReg = 8;      // leading probes held in registers (r <= 31)
+constexpr int kMaxFactors = 9;  // distinct prime factors of p < 2^32
+
+struct SieveArgs {
+	const uint32_t* ext;          // row-extended tables
+	const uint4* probes;          // per probe j: {r, m, ext_base, S}
+	uint32_t np;                  // probes (killable tables, rank order)
+	uint32_t nreg;                // leading probes held in registers
+	uint32_t reg_r[kMaxReg], reg_m[kMaxReg], reg_base[kMaxReg], reg_delta[kMaxReg];
+	const uint2* fprimes;         // {f, barrett m} primes < 2^16 for trial division
+	uint32_t n_fprimes;
+	// row slots: slot s -> owned block ordinal s/100, p = (blk0 + ord*G)*100 + s%100
+	uint64_t p_lo, p_hi, q_start;
+	int mode;
+	uint32_t G;
+	uint64_t blk0;                // first owned block of this launch
+	uint32_t n_slots;
+	const unsigned long long* prefix;  // [n_slots + 1] windows before slot
+	// outputs
+	unsigned long long* hist_probe;    // [np] by probe index
+	unsigned long long* counters;      // [0] pairs_tested, [1] survivors
+	uint32_t* block_rmax;              // [p/100 - blk_lo]
+	uint64_t blk_lo;
+	unsigned long long* surv;          // (p << 32) | q
+	unsigned long long surv_cap;
+};
+
+cudaError_t launch_plan(const SieveArgs& a, unsigned long long* d_prefix, cudaStream_t s);
+cudaError_t launch_sieve(const SieveArgs& a, int grid, cudaStream_t s);
+int sieve_grid(int device, int nreg, size_t smem_bytes);
+size_t sieve_smem_bytes(uint32_t np);
+
+cudaError_t launch_init_blocks(uint32_t* d_block_rmax, uint64_t nblocks, uint64_t blk_lo,
+                               uint32_t G, uint32_t g, cudaStream_t s);
+
+// K3: first-killer rank for explicit pairs.
+cudaError_t launch_classify(const uint64_t* d_pq, uint64_t n, const uint8_t* d_packed,
+                            const uint32_t* d_primes, const uint32_t* d_offsets, uint32_t nprimes,
+                            int32_t* d_out, cudaStream_t s);
+
+}  // namespace cgpu

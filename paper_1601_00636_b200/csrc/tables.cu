@@ -1,0 +1,262 @@
+// K1: residue-table builder for sm_100a.
+//
+// Replaces build_table / build_table_oracle / SieveSet::build
+// (/root/reference/proj/include/cuboid/sievetable.hpp:102-176). All arithmetic
+// is 32-bit with Barrett reduction (common.cuh); tables are produced directly
+// in the reference's packed LSB-first format by warp ballots, so the bytes are
+// identical to the CPU builder's.
+//
+// Grids are 2-D: blockIdx.y selects the prime (jobs sorted by descending r so
+// the heaviest primes are dispatched first), blockIdx.x strides over that
+// prime's work units.
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace cgpu {
+namespace {
+
+constexpr uint32_t kFull = 0xffffffffu;
+
+// Coefficients c4..c0 (c[0]..c[4]) of Q_pq as a monic quintic in s = t^2,
+// reduced to [0, r) -- modpoly.hpp:86-114. Any exact reduction gives the same
+// canonical residues; products of residues are < r^2 < 2^27.
+__device__ __forceinline__ void mod_coeffs(uint32_t p, uint32_t q, uint32_t r, uint32_t m,
+                                           uint32_t c[5])
+{
+	auto md = [r, m](uint32_t x) { return mod_full(x, r, m); };
+	const uint32_t p2 = md(p * p), q2 = md(q * q);
+	const uint32_t p4 = md(p2 * p2), q4 = md(q2 * q2);
+	const uint32_t p6 = md(p4 * p2), q6 = md(q4 * q2);
+	const uint32_t p8 = md(p4 * p4), q8 = md(q4 * q4);
+	c[0] = md(md(2 * q2 + p2) * md(3 * q2 + 2 * r - 2 * p2));
+	c[1] = md(q8 + 10 * md(p2 * q6) + 4 * md(p4 * q4) + 14 * (r - md(p6 * q2)) + p8);
+	const uint32_t in = md(q8 + 14 * (r - md(p2 * q6)) + 4 * md(p4 * q4) + 10 * md(p6 * q2) + p8);
+	c[2] = md(r - md(md(p2 * q2) * in));
+	const uint32_t f1 = md(q2 + 2 * p2), f2 = md(3 * p2 + 2 * r - 2 * q2);
+	c[3] = md(r - md(md(md(p6 * q6) * f1) * f2));
+	c[4] = md(r - md(md(p8 * p2) * md(q8 * q2)));
+}
+
+// Horner in s (modpoly.hpp:116-125) with lazy Barrett: every intermediate
+// stays in [0, 2r), so y = v*s + c < 2r^2 + r < 2^28. Returns v in [0, 2r);
+// Q = 0 mod r iff v == 0 or v == r.
+__device__ __forceinline__ uint32_t horner_lazy(const uint32_t c[5], uint32_t s, uint32_t r,
+                                                uint32_t m)
+{
+	uint32_t v = s + c[0];
+	v = mod_lazy(v * s + c[1], r, m);
+	v = mod_lazy(v * s + c[2], r, m);
+	v = mod_lazy(v * s + c[3], r, m);
+	v = mod_lazy(v * s + c[4], r, m);
+	return v;
+}
+
+// Writes one ballot word covering bits [i0, i0+32) of a table (i0 % 32 == 0)
+// as 4 bytes, clipped to the table's ceil(r^2/8) bytes.
+__device__ __forceinline__ void store_word_bytes(uint8_t* table, uint32_t tbytes, uint32_t i0,
+                                                 uint32_t word, uint32_t lane)
+{
+	if (lane < 4) {
+		const uint32_t bi = (i0 >> 3) + lane;
+		if (bi < tbytes) table[bi] = static_cast<uint8_t>(word >> (8 * lane));
+	}
+}
+
+// Exhaustive cube (sievetable.hpp:102-115 semantics, every t evaluated): one
+// thread per (a,b), all t in [0, r). s = t^2 mod r is hoisted into shared
+// memory and read as a broadcast.
+__global__ void __launch_bounds__(kCubeThreads) k_cube(const PrimeJob* __restrict__ jobs,
+                                                       uint8_t* __restrict__ packed)
+{
+	extern __shared__ uint16_t s_sq[];
+	const PrimeJob job = jobs[blockIdx.y];
+	const uint32_t r = job.r, m = job.m;
+	for (uint32_t t = threadIdx.x; t < r; t += blockDim.x) s_sq[t] = mod_full(t * t, r, m);
+	__syncthreads();
+	const uint32_t rr = r * r;
+	const uint32_t tbytes = (rr + 7) >> 3;
+	const uint32_t lane = threadIdx.x & 31;
+	for (uint32_t base = blockIdx.x * kCubeThreads; base < rr; base += gridDim.x * kCubeThreads) {
+		const uint32_t i = base + threadIdx.x;
+		const bool valid = i < rr;
+		uint32_t a = __umulhi(i, m), b = i - a * r;
+		if (b >= r) { b -= r; ++a; }
+		uint32_t c[5];
+		mod_coeffs(valid ? a : 0, valid ? b : 0, r, m, c);
+		bool hit = false;
+#pragma unroll 4
+		for (uint32_t t = 0; t < r; ++t) {
+			const uint32_t v = horner_lazy(c, s_sq[t], r, m);
+			hit |= (v == 0) | (v == r);
+		}
+		const uint32_t word = __ballot_sync(kFull, valid && !hit);
+		store_word_bytes(packed + job.byte_off, tbytes, base + (threadIdx.x & ~31u), word, lane);
+	}
+}
+
+__device__ __forceinline__ uint32_t pow_mod(uint32_t a, uint32_t e, uint32_t r, uint32_t m)
+{
+	uint32_t x = 1 % r;
+	while (e) {
+		if (e & 1) x = mod_full(x * a, r, m);
+		a = mod_full(a * a, r, m);
+		e >>= 1;
+	}
+	return x;
+}
+
+// Production row 1 (sievetable.hpp:128-132 via row_solvable :91-96, t <= r/2
+// with early exit) and the inverse table used by the permutation
+// (primes.hpp:33-46; here by Fermat). One thread per q.
+__global__ void __launch_bounds__(kRow1Threads) k_row1(const PrimeJob* __restrict__ jobs,
+                                                       uint8_t* __restrict__ row1,
+                                                       uint32_t* __restrict__ inv,
+                                                       unsigned long long* __restrict__ evals)
+{
+	const PrimeJob job = jobs[blockIdx.y];
+	const uint32_t r = job.r, m = job.m;
+	unsigned long long n = 0;
+	for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < r; q += gridDim.x * blockDim.x) {
+		uint32_t c[5];
+		mod_coeffs(1, q, r, m, c);
+		bool solvable = false;
+		for (uint32_t t = 0; t <= r / 2; ++t) {
+			++n;
+			const uint32_t v = horner_lazy(c, mod_full(t * t, r, m), r, m);
+			if (v == 0 || v == r) {
+				solvable = true;
+				break;
+			}
+		}
+		row1[job.aux_off + q] = solvable ? 0 : 1;
+		inv[job.aux_off + q] = q ? pow_mod(q, r - 2, r, m) : 0;
+	}
+	for (int o = 16; o; o >>= 1) n += __shfl_xor_sync(kFull, n, o);
+	if ((threadIdx.x & 31) == 0 && n) atomicAdd(evals, n);
+}
+
+// Production rows a >= 1: row[a][q] = row1[a^{-1} q mod r]; row 0 is zero
+// (sievetable.hpp:133-139). One thread per bit, packed by ballot.
+__global__ void __launch_bounds__(kPermThreads) k_permute(const PrimeJob* __restrict__ jobs,
+                                                          const uint8_t* __restrict__ row1,
+                                                          const uint32_t* __restrict__ inv,
+                                                          uint8_t* __restrict__ packed)
+{
+	const PrimeJob job = jobs[blockIdx.y];
+	const uint32_t r = job.r, m = job.m;
+	const uint32_t rr = r * r, tbytes = (rr + 7) >> 3;
+	const uint32_t lane = threadIdx.x & 31;
+	for (uint32_t base = blockIdx.x * kPermThreads; base < rr; base += gridDim.x * kPermThreads) {
+		const uint32_t i = base + threadIdx.x;
+		uint32_t bit = 0;
+		if (i < rr) {
+			uint32_t a = __umulhi(i, m), q = i - a * r;
+			if (q >= r) { q -= r; ++a; }
+			if (a) bit = row1[job.aux_off + mod_full(inv[job.aux_off + a] * q, r, m)];
+		}
+		const uint32_t word = __ballot_sync(kFull, bit);
+		store_word_bytes(packed + job.byte_off, tbytes, base + (threadIdx.x & ~31u), word, lane);
+	}
+}
+
+// Packed reference tables -> row-extended words (common.cuh ext_row_words):
+// word j of row a holds bits u(a, (32j + l) mod r), l = 0..31. One warp per
+// word; killable[k] is set when any word of table k is nonzero.
+__global__ void __launch_bounds__(kDeriveThreads) k_derive(const PrimeJob* __restrict__ jobs,
+                                                           const uint8_t* __restrict__ packed,
+                                                           uint32_t* __restrict__ ext,
+                                                           uint32_t* __restrict__ killable)
+{
+	const PrimeJob job = jobs[blockIdx.y];
+	const uint32_t r = job.r, m = job.m, S = ext_row_words(r);
+	const uint32_t words = r * S;
+	const uint32_t lane = threadIdx.x & 31;
+	const uint32_t wpb = blockDim.x / 32;
+	const uint8_t* tab = packed + job.byte_off;
+	bool any = false;
+	for (uint32_t w = blockIdx.x * wpb + threadIdx.x / 32; w < words; w += gridDim.x * wpb) {
+		const uint32_t a = w / S, j = w - a * S;
+		const uint32_t q = mod_full(32 * j + lane, r, m);
+		const uint32_t idx = a * r + q;
+		const uint32_t bit = (__ldg(tab + (idx >> 3)) >> (idx & 7)) & 1u;
+		const uint32_t word = __ballot_sync(kFull, bit);
+		if (lane == 0) ext[job.ext_base + w] = word;
+		any |= word != 0;
+	}
+	if (lane == 0 && any) atomicOr(&killable[blockIdx.y], 1u);
+}
+
+// FormatError check (sievetable.hpp:67-79): bits >= r^2 of the last byte of
+// each table must be zero.
+__global__ void k_check_padding(const PrimeJob* __restrict__ jobs, uint32_t njobs,
+                                const uint8_t* __restrict__ packed, uint32_t* __restrict__ bad)
+{
+	for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < njobs; k += gridDim.x * blockDim.x) {
+		const uint32_t r = jobs[k].r;
+		const uint32_t nbits = r * r, tbytes = (nbits + 7) >> 3;
+		const uint32_t used = nbits & 7;
+		if (used) {
+			const uint8_t last = packed[jobs[k].byte_off + tbytes - 1];
+			if (last >> used) atomicOr(bad, 1u);
+		}
+	}
+}
+
+uint32_t grid_x(uint64_t units, uint32_t per_cta, uint32_t cap)
+{
+	const uint64_t x = (units + per_cta - 1) / per_cta;
+	return static_cast<uint32_t>(x < 1 ? 1 : (x > cap ? cap : x));
+}
+
+}  // namespace
+
+// total_ctas = max over jobs of ceil(r^2/256), the x extent.
+cudaError_t launch_cube(const PrimeJob* d_jobs, uint32_t njobs, uint32_t max_rr, uint8_t* d_packed,
+                        cudaStream_t s)
+{
+	if (!njobs) return cudaSuccess;
+	const dim3 grid(grid_x(max_rr, kCubeThreads, 4096), njobs);
+	const size_t smem = sizeof(uint16_t) * kModulusLimit;
+	k_cube<<<grid, kCubeThreads, smem, s>>>(d_jobs, d_packed);
+	return cudaGetLastError();
+}
+
+cudaError_t launch_row1(const PrimeJob* d_jobs, uint32_t njobs, uint32_t max_r, uint8_t* d_row1,
+                        uint32_t* d_inv, unsigned long long* d_evals, cudaStream_t s)
+{
+	if (!njobs) return cudaSuccess;
+	const dim3 grid(grid_x(max_r, kRow1Threads, 128), njobs);
+	k_row1<<<grid, kRow1Threads, 0, s>>>(d_jobs, d_row1, d_inv, d_evals);
+	return cudaGetLastError();
+}
+
+cudaError_t launch_permute(const PrimeJob* d_jobs, uint32_t njobs, uint32_t max_rr,
+                           const uint8_t* d_row1, const uint32_t* d_inv, uint8_t* d_packed,
+                           cudaStream_t s)
+{
+	if (!njobs) return cudaSuccess;
+	const dim3 grid(grid_x(max_rr, kPermThreads, 256), njobs);
+	k_permute<<<grid, kPermThreads, 0, s>>>(d_jobs, d_row1, d_inv, d_packed);
+	return cudaGetLastError();
+}
+
+cudaError_t launch_derive(const PrimeJob* d_jobs, uint32_t njobs, uint64_t max_words,
+                          const uint8_t* d_packed, uint32_t* d_ext, uint32_t* d_killable,
+                          cudaStream_t s)
+{
+	if (!njobs) return cudaSuccess;
+	const dim3 grid(grid_x(max_words, kDeriveThreads / 32, 256), njobs);
+	k_derive<<<grid, kDeriveThreads, 0, s>>>(d_jobs, d_packed, d_ext, d_killable);
+	return cudaGetLastError();
+}
+
+cudaError_t launch_check_padding(const PrimeJob* d_jobs, uint32_t njobs, const uint8_t* d_packed,
+                                 uint32_t* d_bad, cudaStream_t s)
+{
+	if (!njobs) return cudaSuccess;
+	k_check_padding<<<(njobs + 127) / 128, 128, 0, s>>>(d_jobs, njobs, d_packed, d_bad);
+	return cudaGetLastError();
+}
+
+}  // namespace cgpu
