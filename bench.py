@@ -1,0 +1,444 @@
+#!/usr/bin/env python
+"""Benchmark of the modulo-primes cuboid sieve on B200 (driver contract).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload C5|C4|C3]
+    python bench.py --impl reference ...      # the reference CPU path (oracle/_ref)
+
+One "step" = one pass of the hot path over the workload: the (p,q) pair sieve
+of BASELINE.json's config against resident residue tables, with the
+cross-rank reduction of its results (NCCL all-reduce of pair/survivor counts
+and the first-killer histogram, max-reduce of block r_max, gather of survivor
+lists). Rows are split block-cyclically over ranks (p/100 blocks), so the
+total work is fixed as N grows ("strong" scaling).
+
+`value` = pairs sieved per second over the timed steps, inputs resident in HBM,
+device time from CUDA events on the launching stream, max over ranks; L2 is
+flushed between steps. `e2e` = the same metric through the C ABI with HOST
+buffers: each step uploads the reference-format tables (pinned host memory),
+sieves, reduces and reads the reduced results back. `table_build` = BASELINE
+config 2 (exhaustive Q evaluation over Z_r^3 for the first 256 odd primes) in
+Q evals/s. `roofline` uses the INT32 throughput measured on this GPU in the
+same run (cgpu_int32_peak). `cpu_baseline` = the reference itself
+(oracle/_ref, the unmodified headers) on a bounded seed-chosen sample of the
+same workload, on all host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "(p,q) pairs sieved/s"
+SEED = 20160401
+WORKLOADS = {
+    # BASELINE.json configs; C5 is the largest and the headline
+    "C5": dict(k=256, p_lo=100001, p_hi=300000, pairs=24317097730,
+               desc="C5: TRIANGLE sieve 1e5<p<=3e5, 1<=q<p coprime, 256 odd primes 3..1621"),
+    "C4": dict(k=128, p_lo=2, p_hi=100000, pairs=3039650753,
+               desc="C4: TRIANGLE sieve p<=1e5, 1<=q<p coprime, 128 odd primes 3..727"),
+    "C3": dict(k=64, p_lo=2, p_hi=10000, pairs=30397485,
+               desc="C3: TRIANGLE sieve p<=1e4, 1<=q<p coprime, 64 odd primes 3..313"),
+}
+GATHER_CAP = 4096  # survivors per rank gathered inside the step (C3..C5 have 0)
+
+
+# ---- host-side workload constants ------------------------------------------------------
+
+def phi_and_omega(n):
+    """Euler phi and the number of distinct prime factors for 0..n."""
+    phi = np.arange(n + 1, dtype=np.int64)
+    omega = np.zeros(n + 1, dtype=np.int64)
+    for p in range(2, n + 1):
+        if phi[p] == p:
+            phi[p::p] -= phi[p::p] // p
+            omega[p::p] += 1
+    return phi, omega
+
+
+def ops_per_pair(primes, killable, hist, survivors, pairs, p_lo, p_hi):
+    """7 * D_eff + 4 * omega_bar INT32 ops per candidate pair
+    for the reference algorithm (Barrett q mod r + bit probe per probe into a
+    table that can kill, one Barrett divisibility test per distinct prime
+    factor of p for coprimality). D_eff is exact from this run's histogram."""
+    kill_idx = np.cumsum(np.asarray(killable, dtype=np.int64))  # probes made when rank k kills
+    np_ = int(kill_idx[-1]) if len(kill_idx) else 0
+    probes = float(np.dot(np.asarray(hist, dtype=np.float64), kill_idx)) + survivors * np_
+    d_eff = probes / max(pairs, 1)
+    phi, omega = phi_and_omega(p_hi)
+    w = phi[max(p_lo, 2):p_hi + 1].astype(np.float64)
+    omega_bar = float(np.dot(w, omega[max(p_lo, 2):p_hi + 1]) / w.sum())
+    return 7.0 * d_eff + 4.0 * omega_bar, d_eff, omega_bar
+
+
+# ---- clocks -------------------------------------------------------------------------
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = max(mx, float(f[2]))
+            except ValueError:
+                continue
+            for name, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(name)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---- CPU legs (the checker / reference; the product never runs these) ------------------
+
+class CpuReference:
+    """The reference (oracle/_ref: the unmodified headers) TRIANGLE loop --
+    SieveSet::is_unsolvable in rank order, verify_small_region's pattern over
+    q < p -- on a seed-chosen contiguous block of rows of the workload, sized to
+    ~budget_s, on `threads` host threads. Falls back to the C restatement
+    (oracle/cuboid_oracle.c, one thread) if oracle/_ref is absent."""
+
+    def __init__(self, wl, primes, threads):
+        from oracle import ref as refmod
+        self.wl, self.primes = wl, primes
+        span = wl["p_hi"] - wl["p_lo"] + 1
+        self.span = span
+        self.p0 = wl["p_lo"] + (SEED % max(span - 20000, 1))
+        if refmod.available():
+            rs = refmod.RefSet.build(primes)
+            self._run = lambda lo, hi: refmod.triangle(rs, lo, hi, threads, with_sink=False).pairs_tested
+            self.kind, self.cores = "reference", threads
+        else:
+            from oracle import port
+            tb, offs = port.build_set(primes)
+            self._run = lambda lo, hi: port.sieve(tb, primes, offs, lo, hi, port.TRIANGLE)["pairs_tested"]
+            self.kind, self.cores = "port", 1
+        t = time.perf_counter()
+        self._run(self.p0, self.p0 + 19)
+        self.sec_per_row = max(time.perf_counter() - t, 1e-4) / 20
+
+    def sample(self, budget_s):
+        rows = int(min(max(budget_s / self.sec_per_row, 20), min(self.span, 20000)))
+        t = time.perf_counter()
+        pairs = self._run(self.p0, self.p0 + rows - 1)
+        return dict(pairs=pairs, seconds=time.perf_counter() - t, rows=(self.p0, self.p0 + rows - 1),
+                    kind=self.kind, cores=self.cores)
+
+
+def run_reference_arm(args, wl, primes):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    threads = os.cpu_count() or 1
+    per_step = max(1.0, min(6.0, 150.0 / max(args.steps + args.warmup, 1)))
+    samples = []
+    ref = CpuReference(wl, primes, threads)
+    for i in range(args.warmup + args.steps):
+        s = ref.sample(per_step)
+        if i >= args.warmup:
+            samples.append(s)
+    pairs = sum(s["pairs"] for s in samples)
+    secs = sum(s["seconds"] for s in samples)
+    v = pairs / secs
+    s0 = samples[0]
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "pairs/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * secs / len(samples), "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "u32", "data": "synthetic (deterministic enumeration)",
+        "config": {"workload": wl["desc"], "primes": len(primes),
+                   "p_range": [wl["p_lo"], wl["p_hi"]], "mode": "TRIANGLE"},
+        "cpu_baseline": {"value": v, "unit": "pairs/s", "cores": s0["cores"], "kind": s0["kind"],
+                         "sample": f"rows p={s0['rows'][0]}..{s0['rows'][1]} of {wl['desc'].split(':')[0]} "
+                                   f"({s0['pairs']} pairs per step), SieveSet::is_unsolvable rank-ordered "
+                                   f"loop of verify_small_region over q<p, {s0['cores']} threads"},
+        "e2e": {"value": v, "unit": "pairs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---- the B200 arm -----------------------------------------------------------------------
+
+def run_ours(args, wl, primes):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1601_00636_b200 import _native as N
+    from paper_1601_00636_b200.device import Device
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(local)
+    cuda = torch.device("cuda", local)
+    stream = torch.cuda.Stream(device=cuda)  # the context and all torch work share it
+    torch.cuda.set_stream(stream)
+    L = N.lib()
+
+    def allreduce_max(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=cuda)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local])
+        torch.cuda.synchronize()
+
+    dev = Device(local, stream=stream.cuda_stream)
+
+    # INT32 peaks of this GPU (roofline denominators)
+    peaks = (C.c_double * 3)()
+    N.check(L.cgpu_int32_peak(local, peaks))
+    int_peak = {"alu_lop3": peaks[0], "fma_imad": peaks[1], "mixed": peaks[2]}
+
+    # ---- table build (BASELINE config 2): exhaustive Z_r^3, 256 primes --------------
+    from paper_1601_00636_b200.primes import odd_primes
+    P256 = odd_primes(256)
+    tb_ms = []
+    for i in range(3):
+        _, evals = dev.build(P256, N.BUILD_EXHAUSTIVE, download=False)
+        if i:
+            tb_ms.append(dev.timings_ms()["plan"])  # ms[0] = build kernels
+    cube_ms = float(np.mean(tb_ms))
+    tb_evals = sum(r ** 3 for r in P256)
+    prod_t = []
+    for i in range(3):
+        dev.build(P256, N.BUILD_PRODUCTION, download=False)
+        if i:
+            prod_t.append(dev.timings_ms()["plan"])
+    table_build = {
+        "metric": "table-build Q evals/s", "value": tb_evals / (cube_ms * 1e-3), "unit": "evals/s",
+        "config": "C2: first 256 odd primes (3..1621), every (a,b,t) in Z_r^3, sum r^3 = "
+                  f"{tb_evals} evals, 25,869,968 B of tables",
+        "ms": cube_ms, "production_build_ms": float(np.mean(prod_t)),
+        "roofline": {"bound": "int32", "ops_per_eval": 27,
+                     "achieved": 27 * tb_evals / (cube_ms * 1e-3),
+                     "peak": int_peak["mixed"], "unit": "INT32 ops/s",
+                     "frac": 27 * tb_evals / (cube_ms * 1e-3) / int_peak["mixed"]},
+    }
+
+    # ---- resident set for the workload ------------------------------------------------
+    tables, _ = dev.build(primes, N.BUILD_PRODUCTION)
+    killable = dev.killable()
+    n = len(primes)
+    G, g = world, rank
+    nblocks = wl["p_hi"] // 100 - wl["p_lo"] // 100 + 1
+    acc = torch.zeros(2 + n, dtype=torch.int64, device=cuda)  # [pairs, survivors, hist...]
+    brm = torch.zeros(nblocks, dtype=torch.int32, device=cuda)
+    surv = torch.zeros(GATHER_CAP, dtype=torch.int64, device=cuda)
+    gath = torch.zeros(GATHER_CAP * world, dtype=torch.int64, device=cuda)
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=cuda)  # > 126 MB L2
+
+    def launch():
+        N.check(L.cgpu_sieve_launch_dev(
+            dev._ctx, wl["p_lo"], 0, wl["p_hi"], N.TRIANGLE, G, g,
+            C.c_void_p(acc.data_ptr()), C.c_void_p(acc.data_ptr() + 16), C.c_void_p(brm.data_ptr()),
+            nblocks, C.c_void_p(surv.data_ptr()), GATHER_CAP))
+
+    def exchange():
+        if world > 1:
+            dist.all_reduce(acc, op=dist.ReduceOp.SUM)
+            dist.all_reduce(brm, op=dist.ReduceOp.MAX)
+            dist.all_gather_into_tensor(gath, surv)
+
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    for _ in range(args.warmup):
+        launch()
+        exchange()
+    barrier()
+    step_ms, kern_ms, launches = [], [], 0
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            flush.zero_()
+            e0.record(stream)
+            launch()
+            exchange()
+            e1.record(stream)
+            e1.synchronize()
+            step_ms.append(e0.elapsed_time(e1))
+            kern_ms.append(dev.timings_ms()["sieve"])
+            launches += dev.launch_count()
+        barrier()
+    local_ms = float(np.sum(step_ms))
+    total_ms = allreduce_max(local_ms)
+
+    # results of the last step (already reduced across ranks)
+    res = acc.cpu().numpy()
+    pairs, survivors, hist = int(res[0]), int(res[1]), res[2:]
+    parity_ok = (pairs == wl["pairs"] and int(hist.sum()) + survivors == pairs)
+    local_pairs = pairs if world == 1 else None
+
+    # ---- e2e: host tables in, host results out, through the C ABI -------------------------
+    pinned = torch.empty(len(tables), dtype=torch.uint8, pin_memory=True)
+    pinned.numpy()[:] = np.frombuffer(tables, np.uint8)
+    pr = np.ascontiguousarray(primes, dtype=np.uint32)
+    h_acc = torch.empty(2 + n, dtype=torch.int64, pin_memory=True)
+    h_brm = torch.empty(nblocks, dtype=torch.int32, pin_memory=True)
+    h_surv = torch.empty(GATHER_CAP * world, dtype=torch.int64, pin_memory=True)
+
+    def e2e_step():
+        N.check(L.cgpu_tables_load(dev._ctx, pr.ctypes.data_as(C.c_void_p), n,
+                                   C.c_void_p(pinned.data_ptr()), len(tables)))
+        launch()
+        exchange()
+        h_acc.copy_(acc, non_blocking=True)
+        h_brm.copy_(brm, non_blocking=True)
+        h_surv.copy_(gath if world > 1 else surv, non_blocking=True)
+        stream.synchronize()
+
+    for _ in range(args.warmup):
+        e2e_step()
+    barrier()
+    e2e_s = []
+    for _ in range(args.steps):
+        t = time.perf_counter()
+        e2e_step()
+        e2e_s.append(time.perf_counter() - t)
+    barrier()
+    e2e_total = allreduce_max(float(np.sum(e2e_s)))
+    parity_ok = parity_ok and int(h_acc[0]) == wl["pairs"]
+
+    # ---- roofline of the dominant kernel (k_sieve), rank-local ------------------------------
+    if world > 1:  # this rank's own pairs for the per-launch figure
+        N.check(L.cgpu_sieve_launch_dev(
+            dev._ctx, wl["p_lo"], 0, wl["p_hi"], N.TRIANGLE, G, g,
+            C.c_void_p(acc.data_ptr()), C.c_void_p(acc.data_ptr() + 16), C.c_void_p(brm.data_ptr()),
+            nblocks, C.c_void_p(surv.data_ptr()), GATHER_CAP))
+        local_pairs = int(acc[0].item())
+    opp, d_eff, omega_bar = ops_per_pair(primes, killable, hist, survivors, pairs,
+                                         wl["p_lo"], wl["p_hi"])
+    kavg = float(np.mean(kern_ms))
+    achieved = local_pairs * opp / (kavg * 1e-3)
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get("k_sieve", {}).get(wl["desc"][:2], {}).get("dram_bytes")
+        except (ValueError, AttributeError):
+            traffic = None
+    roof = {"bound": "int32", "achieved": achieved, "peak": int_peak["mixed"],
+            "unit": "INT32 ops/s", "frac": achieved / int_peak["mixed"], "traffic": traffic,
+            "kernel": "k_sieve", "kernel_ms": kavg, "ops_per_pair": opp, "d_eff": d_eff,
+            "omega_bar": omega_bar, "pairs_per_launch": local_pairs,
+            "peak_source": "measured in this run (cgpu_int32_peak, IMAD+LOP3 interleaved)",
+            "int32_peaks": int_peak,
+            "note": "ops_per_pair is the reference algorithm's count (SURVEY 8(d)); the kernel "
+                    "is bit-sliced (one probe answers 32 q), so frac can exceed 1"}
+
+    if rank == 0:
+        value = pairs * args.steps / (total_ms * 1e-3)
+        line = {
+            "metric": METRIC, "value": value, "unit": "pairs/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u32",
+            "data": "synthetic (deterministic enumeration of the BASELINE config)",
+            "config": {"workload": wl["desc"], "primes": n, "p_range": [wl["p_lo"], wl["p_hi"]],
+                       "mode": "TRIANGLE", "pairs_per_step": pairs,
+                       "l2": "flushed between steps (512 MiB write)",
+                       "parallelism": f"dp{world}: p/100 blocks block-cyclic over ranks, "
+                                      "NCCL all-reduce of counts/histogram/r_max + survivor all-gather"},
+            "parity": "ok" if parity_ok else "MISMATCH",
+            "e2e": {"value": pairs * args.steps / e2e_total, "unit": "pairs/s",
+                    "h2d_bytes_per_step": len(tables) + 4 * n,
+                    "d2h_bytes_per_step": 8 * (2 + n) + 4 * nblocks + 8 * GATHER_CAP * world,
+                    "ms_per_step": 1e3 * e2e_total / args.steps,
+                    "path": "cgpu_tables_load(host tables) + cgpu_sieve_launch_dev + reduce + D2H"},
+            "gpu_launches": launches,
+            "roofline": roof,
+            "table_build": table_build,
+            "clocks": clk.summary(),
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            s = CpuReference(wl, primes, os.cpu_count() or 1).sample(args.cpu_budget)
+            line["cpu_baseline"] = {
+                "value": s["pairs"] / s["seconds"], "unit": "pairs/s", "cores": s["cores"],
+                "kind": s["kind"],
+                "sample": f"rows p={s['rows'][0]}..{s['rows'][1]} of {wl['desc'].split(':')[0]} "
+                          f"({s['pairs']} pairs, {s['seconds']:.1f} s)"}
+        print(json.dumps(line), flush=True)
+    dev.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=int(os.environ.get("WORLD_SIZE", "1")))
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="C5")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=15.0, help="seconds of CPU sample")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+    from paper_1601_00636_b200.primes import odd_primes
+    wl = WORKLOADS[args.workload]
+    primes = odd_primes(wl["k"])
+    if args.impl == "reference":
+        return run_reference_arm(args, wl, primes)
+    return run_ours(args, wl, primes)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -137,9 +137,30 @@ int cgpu_sieve(cgpu_ctx* ctx, uint64_t p_lo, uint64_t q_start, uint64_t p_hi, in
                uint32_t shard_count, uint32_t shard_index, uint64_t* counts, uint64_t* hist,
                uint32_t* block_rmax, uint64_t block_cap, uint64_t* surv_pq, uint64_t surv_cap);
 
-/* Device time of the last launch's phases, from CUDA events on the context
- * stream: ms[0] = plan kernel, ms[1] = sieve kernel, ms[2] = whole launch. */
+/* Like cgpu_sieve_launch, but results go to CALLER-OWNED device buffers on the
+ * context's device and stay there (e.g. for an NCCL all-reduce across ranks):
+ *   d_counts[2] = {pairs_tested, survivors}
+ *   d_hist[n]   = first-killer counts by rank (n = primes in the set)
+ *   d_block_rmax[block_cap >= p_hi/100 - p_lo/100 + 1], as in cgpu_sieve_results
+ *   d_surv[surv_cap] = survivors as (p << 32) | q, UNSORTED; d_counts[1] may
+ *                   exceed surv_cap (only the first surv_cap are stored).
+ * Asynchronous on the context stream. */
+int cgpu_sieve_launch_dev(cgpu_ctx* ctx, uint64_t p_lo, uint64_t q_start, uint64_t p_hi, int mode,
+                          uint32_t shard_count, uint32_t shard_index, uint64_t* d_counts,
+                          uint64_t* d_hist, uint32_t* d_block_rmax, uint64_t block_cap,
+                          uint64_t* d_surv, uint64_t surv_cap);
+
+/* Device time of the last sieve launch or table build, from CUDA events on the
+ * context stream (waits for them). Sieve: ms[0] = init + first plan kernel,
+ * ms[1] = sieve kernel(s), ms[2] = whole launch. Table build: ms[0] = build
+ * kernels (cube, or row-1 + permute), ms[1] = device-layout derivation,
+ * ms[2] = both. */
 int cgpu_last_timings(cgpu_ctx* ctx, float* ms3);
+
+/* Measured INT32 throughput of `device` in thread-ops/s: ops3[0] = LOP3 chains
+ * (ALU pipe), ops3[1] = IMAD chains (FMA pipe), ops3[2] = both interleaved
+ * (the issue-bound ceiling). The roofline denominators of the bench. */
+int cgpu_int32_peak(int device, double* ops3);
 
 /* Number of kernels the last cgpu_sieve_launch / cgpu_tables_* enqueued. */
 int cgpu_last_launch_count(cgpu_ctx* ctx, uint32_t* n);

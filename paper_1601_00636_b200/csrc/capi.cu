@@ -141,9 +141,10 @@ struct cgpu_ctx {
 	uint32_t n_fprimes = 0;
 
 	// sieve buffers
-	DevBuf<unsigned long long> hist_probe, counters, surv, prefix;
+	DevBuf<unsigned long long> hist, counters, surv, prefix;
+	DevBuf<uint32_t> d_probe_rank;
 	DevBuf<uint32_t> block_rmax;
-	bool launched = false;
+	bool launched = false, results_internal = false, timed = false;
 	uint64_t last_nblocks = 0, last_surv_cap = 0;
 	cudaEvent_t ev[3] = {};
 	float timings[3] = {};
@@ -329,10 +330,14 @@ int finalize_set(cgpu_ctx* c)
 		++c->nreg;
 	}
 	CK(c->probes.ensure(c->np));
-	if (c->np)
+	CK(c->d_probe_rank.ensure(c->np));
+	if (c->np) {
 		CK(cudaMemcpyAsync(c->probes.p, pr.data(), sizeof(uint4) * c->np, cudaMemcpyHostToDevice,
 		                   c->stream));
-	CK(c->hist_probe.ensure(c->np));
+		CK(cudaMemcpyAsync(c->d_probe_rank.p, c->probe_rank.data(), 4ull * c->np,
+		                   cudaMemcpyHostToDevice, c->stream));
+	}
+	CK(c->hist.ensure(n));
 	const size_t smem = sieve_smem_bytes(c->np);
 	if (smem > 220 * 1024)
 		return set_err(CGPU_ERR_INVALID, "too many probe primes for the sieve's shared memory");
@@ -382,9 +387,11 @@ int cgpu_tables_build(cgpu_ctx* c, const uint32_t* primes, uint32_t n, int algor
 		                   c->stream));
 		CK(cudaMemsetAsync(c->packed.p, 0, c->total_bytes, c->stream));
 		const uint32_t rmax = byr.front().r;
+		CK(cudaEventRecord(c->ev[0], c->stream));
 		if (algorithm == CGPU_BUILD_EXHAUSTIVE) {
 			CK(launch_cube(c->jobs_build.p, n, rmax * rmax, c->packed.p, c->stream));
 			c->launches += 1;
+			CK(cudaEventRecord(c->ev[1], c->stream));
 			for (auto r : c->primes) evals += static_cast<uint64_t>(r) * r * r;
 		} else {
 			uint64_t aux = 0;
@@ -397,13 +404,19 @@ int cgpu_tables_build(cgpu_ctx* c, const uint32_t* primes, uint32_t n, int algor
 			CK(launch_permute(c->jobs_build.p, n, rmax * rmax, c->row1.p, c->inv.p, c->packed.p,
 			                  c->stream));
 			c->launches += 2;
+			CK(cudaEventRecord(c->ev[1], c->stream));
 			unsigned long long ev = 0;
 			CK(cudaMemcpyAsync(&ev, c->evals.p, 8, cudaMemcpyDeviceToHost, c->stream));
 			CK(cudaStreamSynchronize(c->stream));
 			evals = ev;
 		}
 	}
+	c->timed = false;
 	if (int rc = finalize_set(c)) return rc;
+	if (n) {  // timings: [0] build kernels, [1] device layout derivation, [2] both
+		CK(cudaEventRecord(c->ev[2], c->stream));
+		c->timed = true;
+	}
 	if (out_bytes && c->total_bytes) {
 		CK(cudaMemcpyAsync(out_bytes, c->packed.p, c->total_bytes, cudaMemcpyDeviceToHost, c->stream));
 		CK(cudaStreamSynchronize(c->stream));
@@ -479,8 +492,13 @@ int cgpu_build_tables(int device, const uint32_t* primes, uint32_t n, int algori
 	return rc;
 }
 
-int cgpu_sieve_launch(cgpu_ctx* c, uint64_t p_lo, uint64_t q_start, uint64_t p_hi, int mode,
-                      uint32_t G, uint32_t g, uint64_t surv_cap)
+}  // extern "C"
+
+namespace {
+
+// Validation shared by both launch entry points (engine.hpp:152-161 codes).
+int check_launch(cgpu_ctx* c, uint64_t p_lo, uint64_t q_start, uint64_t p_hi, int mode, uint32_t G,
+                 uint32_t g)
 {
 	if (!c) return set_err(CGPU_ERR_INVALID, "null ctx");
 	if (!c->loaded || c->primes.empty()) return set_err(CGPU_NOT_LOADED, "tables not loaded");
@@ -500,22 +518,31 @@ int cgpu_sieve_launch(cgpu_ctx* c, uint64_t p_lo, uint64_t q_start, uint64_t p_h
 		if (q_start) return set_err(CGPU_ERR_INVALID, "TRIANGLE mode sieves whole rows (q_start must be 0)");
 		if (p_hi > 0xffffffffull) return set_err(CGPU_P_ABOVE_LIMIT, "p above 2^32");
 	}
-	CK(cudaSetDevice(c->device));
+	return CGPU_OK;
+}
+
+uint64_t launch_blocks(uint64_t p_lo, uint64_t p_hi)
+{
+	return p_hi < p_lo ? 0 : p_hi / 100 - p_lo / 100 + 1;
+}
+
+// Enqueues init + (plan, sieve) per chunk of row slots on the context stream,
+// writing into the given device buffers. Events ev[0..2] bracket the launch.
+int enqueue_sieve(cgpu_ctx* c, uint64_t p_lo, uint64_t q_start, uint64_t p_hi, int mode, uint32_t G,
+                  uint32_t g, unsigned long long* d_counts, unsigned long long* d_hist,
+                  uint32_t* d_block_rmax, unsigned long long* d_surv, uint64_t surv_cap)
+{
 	c->launched = false;
 	c->launches = 0;
 	const bool empty = p_hi < p_lo;
 	const uint64_t blk_lo = p_lo / 100;
-	const uint64_t nblocks = empty ? 0 : p_hi / 100 - blk_lo + 1;
-	CK(c->hist_probe.ensure(c->np));
-	CK(c->counters.ensure(2));
-	CK(c->block_rmax.ensure(nblocks));
-	CK(c->surv.ensure(surv_cap));
-	CK(cudaMemsetAsync(c->hist_probe.p, 0, 8ull * c->np, c->stream));
-	CK(cudaMemsetAsync(c->counters.p, 0, 16, c->stream));
-	CK(launch_init_blocks(c->block_rmax.p, nblocks, blk_lo, G, g, c->stream));
-	++c->launches;
+	const uint64_t nblocks = launch_blocks(p_lo, p_hi);
 	CK(cudaEventRecord(c->ev[0], c->stream));
-	CK(cudaEventRecord(c->ev[1], c->stream));
+	CK(cudaMemsetAsync(d_hist, 0, 8ull * c->primes.size(), c->stream));
+	CK(cudaMemsetAsync(d_counts, 0, 16, c->stream));
+	CK(launch_init_blocks(d_block_rmax, nblocks, blk_lo, G, g, c->stream));
+	if (nblocks) ++c->launches;
+	bool ev1 = false;
 
 	SieveArgs a{};
 	a.ext = c->ext.p;
@@ -535,68 +562,100 @@ int cgpu_sieve_launch(cgpu_ctx* c, uint64_t p_lo, uint64_t q_start, uint64_t p_h
 	a.q_start = q_start;
 	a.mode = mode;
 	a.G = G;
-	a.hist_probe = c->hist_probe.p;
-	a.counters = c->counters.p;
-	a.block_rmax = c->block_rmax.p;
+	a.hist = d_hist;
+	a.probe_rank = c->d_probe_rank.p;
+	a.counters = d_counts;
+	a.block_rmax = d_block_rmax;
 	a.blk_lo = blk_lo;
-	a.surv = c->surv.p;
+	a.surv = d_surv;
 	a.surv_cap = surv_cap;
 
-	if (!empty && c->np) {
+	if (!empty) {  // np == 0 (no table can kill): every candidate survives
 		// owned blocks: b in [blk_lo, blk_hi] with b % G == g
 		const uint64_t blk_hi = p_hi / 100;
 		const uint64_t first = blk_lo + ((g + G - blk_lo % G) % G);
 		const uint64_t owned = first <= blk_hi ? (blk_hi - first) / G + 1 : 0;
 		CK(c->prefix.ensure(static_cast<size_t>(std::min<uint64_t>(owned, kBlocksPerLaunch)) * 100 + 1));
-		bool first_chunk = true;
 		for (uint64_t ob = 0; ob < owned; ob += kBlocksPerLaunch) {
 			const uint64_t nb = std::min<uint64_t>(kBlocksPerLaunch, owned - ob);
 			a.blk0 = first + ob * G;
 			a.n_slots = static_cast<uint32_t>(nb * 100);
 			a.prefix = c->prefix.p;
 			CK(launch_plan(a, c->prefix.p, c->stream));
-			if (first_chunk) CK(cudaEventRecord(c->ev[1], c->stream));
-			first_chunk = false;
+			if (!ev1) CK(cudaEventRecord(c->ev[1], c->stream));  // sieve time excludes the first plan
+			ev1 = true;
 			CK(launch_sieve(a, c->grid[c->nreg], c->stream));
 			c->launches += 2;
 		}
 	}
+	if (!ev1) CK(cudaEventRecord(c->ev[1], c->stream));
 	CK(cudaEventRecord(c->ev[2], c->stream));
+	c->timed = true;
 	c->last_nblocks = nblocks;
 	c->last_surv_cap = surv_cap;
 	c->launched = true;
 	return CGPU_OK;
 }
 
+}  // namespace
+
+extern "C" {
+
+int cgpu_sieve_launch(cgpu_ctx* c, uint64_t p_lo, uint64_t q_start, uint64_t p_hi, int mode,
+                      uint32_t G, uint32_t g, uint64_t surv_cap)
+{
+	if (int rc = check_launch(c, p_lo, q_start, p_hi, mode, G, g)) return rc;
+	CK(cudaSetDevice(c->device));
+	CK(c->hist.ensure(c->primes.size()));
+	CK(c->counters.ensure(2));
+	CK(c->block_rmax.ensure(launch_blocks(p_lo, p_hi)));
+	CK(c->surv.ensure(surv_cap));
+	c->results_internal = true;
+	return enqueue_sieve(c, p_lo, q_start, p_hi, mode, G, g, c->counters.p, c->hist.p, c->block_rmax.p,
+	                     c->surv.p, surv_cap);
+}
+
+int cgpu_sieve_launch_dev(cgpu_ctx* c, uint64_t p_lo, uint64_t q_start, uint64_t p_hi, int mode,
+                          uint32_t G, uint32_t g, uint64_t* d_counts, uint64_t* d_hist,
+                          uint32_t* d_block_rmax, uint64_t block_cap, uint64_t* d_surv,
+                          uint64_t surv_cap)
+{
+	if (int rc = check_launch(c, p_lo, q_start, p_hi, mode, G, g)) return rc;
+	if (!d_counts || !d_hist || (!d_block_rmax && launch_blocks(p_lo, p_hi)) || (!d_surv && surv_cap))
+		return set_err(CGPU_ERR_INVALID, "null device output buffer");
+	if (block_cap < launch_blocks(p_lo, p_hi))
+		return set_err(CGPU_ERR_CAPACITY, "block_rmax buffer too small");
+	CK(cudaSetDevice(c->device));
+	c->results_internal = false;
+	return enqueue_sieve(c, p_lo, q_start, p_hi, mode, G, g,
+	                     reinterpret_cast<unsigned long long*>(d_counts),
+	                     reinterpret_cast<unsigned long long*>(d_hist), d_block_rmax,
+	                     reinterpret_cast<unsigned long long*>(d_surv), surv_cap);
+}
+
 int cgpu_sieve_results(cgpu_ctx* c, uint64_t* counts, uint64_t* hist, uint32_t* block_rmax,
                        uint64_t block_cap, uint64_t* surv_pq, uint64_t surv_cap)
 {
 	if (!c) return set_err(CGPU_ERR_INVALID, "null ctx");
-	if (!c->launched) return set_err(CGPU_ERR_INVALID, "no sieve launched");
+	if (!c->launched || !c->results_internal)
+		return set_err(CGPU_ERR_INVALID, "no sieve launched into context buffers");
 	CK(cudaSetDevice(c->device));
 	unsigned long long cnt[2] = {0, 0};
-	std::vector<unsigned long long> hp(c->np);
+	std::vector<unsigned long long> hp(c->primes.size());
 	CK(cudaMemcpyAsync(cnt, c->counters.p, 16, cudaMemcpyDeviceToHost, c->stream));
-	if (c->np)
-		CK(cudaMemcpyAsync(hp.data(), c->hist_probe.p, 8ull * c->np, cudaMemcpyDeviceToHost, c->stream));
+	if (!hp.empty())
+		CK(cudaMemcpyAsync(hp.data(), c->hist.p, 8ull * hp.size(), cudaMemcpyDeviceToHost, c->stream));
 	if (block_rmax && c->last_nblocks) {
 		if (block_cap < c->last_nblocks) return set_err(CGPU_ERR_CAPACITY, "block_rmax buffer too small");
 		CK(cudaMemcpyAsync(block_rmax, c->block_rmax.p, 4ull * c->last_nblocks, cudaMemcpyDeviceToHost,
 		                   c->stream));
 	}
 	CK(cudaStreamSynchronize(c->stream));
-	float ms = 0;
-	if (cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]) == cudaSuccess) c->timings[0] = ms;
-	if (cudaEventElapsedTime(&ms, c->ev[1], c->ev[2]) == cudaSuccess) c->timings[1] = ms;
-	if (cudaEventElapsedTime(&ms, c->ev[0], c->ev[2]) == cudaSuccess) c->timings[2] = ms;
 	if (counts) {
 		counts[0] = cnt[0];
 		counts[1] = cnt[1];
 	}
-	if (hist) {
-		std::fill(hist, hist + c->primes.size(), 0ull);
-		for (uint32_t j = 0; j < c->np; ++j) hist[c->probe_rank[j]] = hp[j];
-	}
+	if (hist) std::copy(hp.begin(), hp.end(), hist);
 	int rc = CGPU_OK;
 	if (surv_pq && cnt[1]) {
 		const uint64_t stored = std::min<uint64_t>(cnt[1], c->last_surv_cap);
@@ -625,7 +684,26 @@ int cgpu_sieve(cgpu_ctx* c, uint64_t p_lo, uint64_t q_start, uint64_t p_hi, int 
 int cgpu_last_timings(cgpu_ctx* c, float* ms3)
 {
 	if (!c || !ms3) return set_err(CGPU_ERR_INVALID, "null argument");
+	if (c->timed) {
+		CK(cudaSetDevice(c->device));
+		CK(cudaEventSynchronize(c->ev[2]));
+		float ms = 0;
+		if (cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]) == cudaSuccess) c->timings[0] = ms;
+		if (cudaEventElapsedTime(&ms, c->ev[1], c->ev[2]) == cudaSuccess) c->timings[1] = ms;
+		if (cudaEventElapsedTime(&ms, c->ev[0], c->ev[2]) == cudaSuccess) c->timings[2] = ms;
+	}
 	std::memcpy(ms3, c->timings, sizeof c->timings);
+	return CGPU_OK;
+}
+
+int cgpu_int32_peak(int device, double* ops3)
+{
+	if (!ops3) return set_err(CGPU_ERR_INVALID, "null argument");
+	int count = 0;
+	if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0)
+		return set_err(CGPU_ERR_NO_DEVICE, "no CUDA device visible: cuboid_gpu has no CPU fallback");
+	CK(cudaSetDevice(device));
+	CK(run_int_peak(device, ops3));
 	return CGPU_OK;
 }
 

@@ -70,7 +70,8 @@ struct SieveArgs {
 	uint32_t n_slots;
 	const unsigned long long* prefix;  // [n_slots + 1] windows before slot
 	// outputs
-	unsigned long long* hist_probe;    // [np] by probe index
+	unsigned long long* hist;          // [n primes] first-killer counts by rank
+	const uint32_t* probe_rank;        // [np] rank of probe j
 	unsigned long long* counters;      // [0] pairs_tested, [1] survivors
 	uint32_t* block_rmax;              // [p/100 - blk_lo]
 	uint64_t blk_lo;
@@ -90,5 +91,8 @@ cudaError_t launch_init_blocks(uint32_t* d_block_rmax, uint64_t nblocks, uint64_
 cudaError_t launch_classify(const uint64_t* d_pq, uint64_t n, const uint8_t* d_packed,
                             const uint32_t* d_primes, const uint32_t* d_offsets, uint32_t nprimes,
                             int32_t* d_out, cudaStream_t s);
+
+// INT32 pipe peaks (peak.cu): out = {LOP3-only, IMAD-only, mixed} thread-ops/s.
+cudaError_t run_int_peak(int device, double out[3]);
 
 }  // namespace cgpu

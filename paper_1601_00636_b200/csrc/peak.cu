@@ -1,0 +1,77 @@
+// Measured INT32 denominators for the roofline (MEASURED_PEAKS.json has only
+// HBM and bf16): chains of LOP3 (ALU pipe), IMAD (FMA pipe) and both
+// interleaved, over a full-chip grid, timed with CUDA events.
+
+#include "../../include/cuboid_gpu.h"
+#include "kernels.cuh"
+
+namespace cgpu {
+namespace {
+
+constexpr int kChains = 8;
+constexpr int kIters = 2048;
+constexpr int kPeakThreads = 256;
+
+// mode 0: LOP3 only; 1: IMAD only; 2: one IMAD + one LOP3 per step.
+template <int MODE>
+__global__ void __launch_bounds__(kPeakThreads) k_int_peak(uint32_t seed, uint32_t* sink)
+{
+	uint32_t x[kChains], y[kChains];
+#pragma unroll
+	for (int i = 0; i < kChains; ++i) {
+		x[i] = seed + threadIdx.x * 7 + i;
+		y[i] = seed ^ (blockIdx.x * 13 + i);
+	}
+	const uint32_t a = seed | 1, b = seed >> 3, c = seed * 5;
+	for (int it = 0; it < kIters; ++it) {
+#pragma unroll
+		for (int i = 0; i < kChains; ++i) {
+			if (MODE != 0) asm volatile("mad.lo.u32 %0, %0, %1, %2;" : "+r"(x[i]) : "r"(a), "r"(b));
+			if (MODE != 1)
+				asm volatile("lop3.b32 %0, %0, %1, %2, 0x96;" : "+r"(y[i]) : "r"(c), "r"(x[i]));
+		}
+	}
+	uint32_t acc = 0;
+#pragma unroll
+	for (int i = 0; i < kChains; ++i) acc ^= x[i] ^ y[i];
+	if (acc == 0x9e3779b9u) sink[0] = acc;  // keeps the chains live
+}
+
+}  // namespace
+
+cudaError_t run_int_peak(int device, double out[3])
+{
+	int sms = 0;
+	cudaError_t e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+	if (e != cudaSuccess) return e;
+	uint32_t* sink = nullptr;
+	if ((e = cudaMalloc(&sink, 4)) != cudaSuccess) return e;
+	cudaEvent_t t0, t1;
+	cudaEventCreate(&t0);
+	cudaEventCreate(&t1);
+	const int grid = sms * 8;  // 8 CTAs x 8 warps = 64 warps per SM
+	const double threads = static_cast<double>(grid) * kPeakThreads;
+	void (*fns[3])(uint32_t, uint32_t*) = {k_int_peak<0>, k_int_peak<1>, k_int_peak<2>};
+	const double ops_per_thread[3] = {1.0 * kIters * kChains, 1.0 * kIters * kChains,
+	                                  2.0 * kIters * kChains};
+	for (int m = 0; m < 3 && e == cudaSuccess; ++m) {
+		float best = 1e30f;
+		for (int rep = 0; rep < 5; ++rep) {
+			cudaEventRecord(t0);
+			fns[m]<<<grid, kPeakThreads>>>(0x1234567u + rep, sink);
+			cudaEventRecord(t1);
+			if ((e = cudaEventSynchronize(t1)) != cudaSuccess) break;
+			float ms = 0;
+			cudaEventElapsedTime(&ms, t0, t1);
+			if (rep && ms < best) best = ms;  // rep 0 is warm-up
+		}
+		out[m] = threads * ops_per_thread[m] / (best * 1e-3);
+	}
+	if (e == cudaSuccess) e = cudaGetLastError();
+	cudaEventDestroy(t0);
+	cudaEventDestroy(t1);
+	cudaFree(sink);
+	return e;
+}
+
+}  // namespace cgpu

@@ -74,6 +74,18 @@ __device__ __forceinline__ uint64_t row_windows(const RowBounds& b)
 	return b.qhi >= b.qlo ? (b.qhi - b.qlo + 32) / 32 : 0;
 }
 
+// Work units of a row for load balancing: its 32-q windows plus a fixed
+// charge for the per-row setup (trial division of p, per-prime row bases),
+// measured at ~150 window-equivalents. Without it the warps that own the
+// many short rows at small p straggle (C4: one SM busy 5x longer than the rest).
+constexpr uint32_t kRowCost = 160;
+
+__device__ __forceinline__ uint64_t row_units(const RowBounds& b)
+{
+	const uint64_t w = row_windows(b);
+	return w ? w + kRowCost : 0;
+}
+
 // Plan: exclusive prefix of windows over row slots (one CTA).
 __global__ void __launch_bounds__(1024) k_plan(const SieveArgs a, unsigned long long* prefix)
 {
@@ -83,7 +95,7 @@ __global__ void __launch_bounds__(1024) k_plan(const SieveArgs a, unsigned long 
 	const uint32_t s0 = threadIdx.x * per;
 	const uint32_t s1 = min(n, s0 + per);
 	unsigned long long sum = 0;
-	for (uint32_t s = s0; s < s1; ++s) sum += row_windows(slot_row(a, s));
+	for (uint32_t s = s0; s < s1; ++s) sum += row_units(slot_row(a, s));
 	s_part[threadIdx.x] = sum;
 	__syncthreads();
 	for (uint32_t off = 1; off < blockDim.x; off <<= 1) {
@@ -95,7 +107,7 @@ __global__ void __launch_bounds__(1024) k_plan(const SieveArgs a, unsigned long 
 	unsigned long long run = s_part[threadIdx.x] - sum;
 	for (uint32_t s = s0; s < s1; ++s) {
 		prefix[s] = run;
-		run += row_windows(slot_row(a, s));
+		run += row_units(slot_row(a, s));
 	}
 	if (threadIdx.x == blockDim.x - 1) prefix[n] = s_part[blockDim.x - 1];
 }
@@ -149,14 +161,18 @@ __global__ void __launch_bounds__(kSieveThreads) k_sieve(const SieveArgs a)
 			++slot;
 			continue;
 		}
-		const RowBounds rb = slot_row(a, slot);
+		// this warp's share of the row's units; the first kRowCost are the
+		// setup charge, the rest map 1:1 to windows
+		const unsigned long long u0 = ws - rs, u1 = min(we, re) - rs;
+		ws = min(we, re);
+		const uint32_t cur = slot++;
+		if (u1 <= kRowCost) continue;
+		const uint32_t w0 = static_cast<uint32_t>(u0 > kRowCost ? u0 - kRowCost : 0);
+		const uint32_t w1 = static_cast<uint32_t>(u1 - kRowCost);
+		const RowBounds rb = slot_row(a, cur);
 		const uint32_t p = static_cast<uint32_t>(rb.p);
 		const uint32_t qlo = static_cast<uint32_t>(rb.qlo);
 		const uint32_t qhi = static_cast<uint32_t>(rb.qhi);
-		const uint32_t w0 = static_cast<uint32_t>(ws - rs);
-		const uint32_t w1 = static_cast<uint32_t>(min(we, re) - rs);
-		ws = min(we, re);
-		++slot;
 
 		// ---- row setup: distinct prime factors of p (trial division) ----
 		uint32_t fac[kMaxFactors];
@@ -321,7 +337,7 @@ __global__ void __launch_bounds__(kSieveThreads) k_sieve(const SieveArgs a)
 	if (lane == 0 && pairs) atomicAdd(&s_pairs, pairs);
 	__syncthreads();
 	for (uint32_t j = threadIdx.x; j < a.np; j += blockDim.x)
-		if (s_hist[j]) atomicAdd(&a.hist_probe[j], s_hist[j]);
+		if (s_hist[j]) atomicAdd(&a.hist[__ldg(a.probe_rank + j)], s_hist[j]);
 	if (threadIdx.x == 0 && s_pairs) atomicAdd(&a.counters[0], s_pairs);
 }
 

@@ -1,0 +1,329 @@
+"""Host-side mirror of the reference's hot-path API, running on the B200.
+
+Same names, argument meaning and error behaviour as the reference's header-only
+C++ API (paths relative to /root/reference/proj/include/cuboid):
+
+    build_table(r)                     sievetable.hpp:123-141
+    SieveSet.build(primes)             sievetable.hpp:159-176
+    SieveSet.build_default()           sievetable.hpp:178-179
+    SieveSet.is_unsolvable(rank,p,q)   sievetable.hpp:199-205
+    scan(set, start, p_end, sink, opt) engine.hpp:195-295
+    ScanStats (+ merge)                engine.hpp:105-135
+    ScanEvent / ScanSink               engine.hpp:97-103
+    ScanOptions                        engine.hpp:144-149
+    ScanRejected(code)                 engine.hpp:163-167
+    q_bounds(p)                        region.hpp:49-63
+
+Every table build and every sieve runs in libcuboid_gpu.so (sm_100a) through
+the C ABI of include/cuboid_gpu.h; there is no CPU fallback. The exact final
+check of survivors (verify_pair, engine.hpp:66-95, GMP) stays on the CPU in
+the reference; pass it as `verifier` to have each ScanEvent carry its verdict,
+exactly as scan() does when a sink is set (engine.hpp:272-277).
+"""
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, field
+from typing import Callable, Optional
+
+import numpy as np
+
+from . import _native as N
+from .device import Device, q_bounds as _q_bounds
+from .primes import default_primes
+
+MODULUS_LIMIT = 9697                  # primes.hpp:12
+REGION_CROSSOVER = 152                # region.hpp:41
+P_LIMIT_32BIT = ((1 << 32) - 1) // 59  # region.hpp:43-44: 59p < 2^32
+P_LIMIT_64BIT = ((1 << 64) - 1) // 59
+
+
+class ScanRejected(RuntimeError):
+    """engine.hpp:163-167; code in {2,3,4,5,6} (engine.hpp:5-12)."""
+
+    def __init__(self, code: int):
+        super().__init__(f"scan rejected with code {code}")
+        self.code = code
+
+
+class FormatError(ValueError):
+    """sievetable.hpp:37-39."""
+
+
+_devices: dict[int, Device] = {}
+
+
+def device(index: int = 0) -> Device:
+    """The process's context on GPU `index` (one process per GPU)."""
+    d = _devices.get(index)
+    if d is None:
+        d = _devices[index] = Device(index)
+    return d
+
+
+def q_bounds(p: int):
+    """(q_low, q_high) of row p (region.hpp:49-63)."""
+    return _q_bounds(p)
+
+
+@dataclass
+class BitTable:
+    """sievetable.hpp:46-55: r and ceil(r^2/8) LSB-first bytes."""
+    r: int
+    bytes: bytes
+
+    def bit(self, p: int, q: int) -> bool:
+        i = p * self.r + q
+        return bool((self.bytes[i >> 3] >> (i & 7)) & 1)
+
+
+def build_table(r: int, dev: int = 0) -> BitTable:
+    """One table, built on the GPU (replaces build_table, sievetable.hpp:123-141).
+    ValueError (std::invalid_argument) for a modulus that is not a prime < 9697."""
+    try:
+        tb, _ = device(dev).build([r], N.BUILD_PRODUCTION)
+    except N.CudaSieveError as e:
+        if e.code == N.ERR_INVALID:
+            raise ValueError("bit table modulus must be a prime below 9697") from e
+        raise
+    return BitTable(r, tb)
+
+
+class SieveSet:
+    """Concatenated tables + prime index, resident on one GPU (sievetable.hpp:151-227)."""
+
+    def __init__(self, primes, tables: bytes, offsets, dev: int):
+        self._primes = [int(x) for x in primes]
+        self._tables = tables
+        self._offsets = [int(x) for x in offsets]
+        self._dev = dev
+
+    # -- construction ------------------------------------------------------
+    @classmethod
+    def build(cls, primes, dev: int = 0, algorithm: int = N.BUILD_PRODUCTION) -> "SieveSet":
+        """SieveSet::build (sievetable.hpp:159-176): ValueError for an unordered
+        or non-prime list (std::invalid_argument), OverflowError past 2^32 bytes."""
+        primes = [int(x) for x in primes]
+        d = device(dev)
+        d._owner = None
+        try:
+            tb, _ = d.build(primes, algorithm)
+        except N.CudaSieveError as e:
+            if e.code == N.ERR_INVALID:
+                raise ValueError(str(e)) from e
+            if e.code == N.ERR_OVERFLOW:
+                raise OverflowError(str(e)) from e
+            raise
+        s = cls(primes, tb, d.offsets, dev)
+        d._owner = id(s)
+        return s
+
+    @classmethod
+    def build_default(cls, dev: int = 0) -> "SieveSet":
+        return cls.build(default_primes(), dev)
+
+    @classmethod
+    def from_parts(cls, primes, tables: bytes, dev: int = 0) -> "SieveSet":
+        """Reference-format bytes (load_sieve, sievetable.hpp:254-292) made resident.
+        FormatError for a length mismatch or nonzero padding bits."""
+        primes = [int(x) for x in primes]
+        d = device(dev)
+        d._owner = None
+        try:
+            d.load(primes, tables)
+        except N.CudaSieveError as e:
+            if e.code in (N.ERR_FORMAT, N.ERR_INVALID):
+                raise FormatError(str(e)) from e
+            raise
+        s = cls(primes, bytes(tables), d.offsets, dev)
+        d._owner = id(s)
+        return s
+
+    # -- queries (sievetable.hpp:181-205) ----------------------------------
+    def empty(self) -> bool:
+        return not self._primes
+
+    def prime_count(self) -> int:
+        return len(self._primes)
+
+    def prime_at(self, rank: int) -> int:
+        if not 0 <= rank < len(self._primes):
+            raise IndexError("rank out of range")
+        return self._primes[rank]
+
+    def primes(self):
+        return list(self._primes)
+
+    def index(self):
+        return list(zip(self._primes, self._offsets))
+
+    def tables(self) -> bytes:
+        return self._tables
+
+    def rank_of(self, r: int):
+        return self._primes.index(r) if r in self._primes else None
+
+    def table_at(self, rank: int) -> BitTable:
+        r = self.prime_at(rank)
+        o = self._offsets[rank]
+        return BitTable(r, self._tables[o:o + (r * r + 7) // 8])
+
+    def is_unsolvable(self, rank: int, p: int, q: int) -> bool:
+        r = self.prime_at(rank)
+        i = (p % r) * r + (q % r)
+        return bool((self._tables[self._offsets[rank] + (i >> 3)] >> (i & 7)) & 1)
+
+    # -- device residency --------------------------------------------------
+    def resident(self) -> Device:
+        """The device context with this set loaded (re-uploads if another set
+        was made resident on the same GPU since)."""
+        d = device(self._dev)
+        if getattr(d, "_owner", None) != id(self):
+            d.load(self._primes, self._tables)
+            d._owner = id(self)
+        return d
+
+
+@dataclass
+class ScanOptions:
+    """engine.hpp:144-149 (hooks are not supported by the device scan)."""
+    small_p: bool = False
+    p_limit: int = P_LIMIT_32BIT
+    batch_pairs: int = 1 << 16
+
+
+@dataclass
+class ScanEvent:
+    p: int
+    q: int
+    verdict: object = None
+
+
+@dataclass
+class ScanStats:
+    """engine.hpp:105-135."""
+    pairs_tested: int = 0
+    survivors: int = 0
+    kill_histogram: dict = field(default_factory=dict)   # prime -> first-kill count
+    block_r_max: dict = field(default_factory=dict)      # p // 100 -> max killing prime, 1 if none
+    elapsed: float = 0.0                                 # seconds
+    resume_p: int = 0
+    resume_q: int = 0
+    stopped: bool = False
+    survivor_pairs: list = field(default_factory=list)   # [(p, q)] ascending
+
+    def histogram_total(self) -> int:
+        return sum(self.kill_histogram.values())
+
+    def merge(self, o: "ScanStats") -> None:
+        self.pairs_tested += o.pairs_tested
+        self.survivors += o.survivors
+        for r, k in o.kill_histogram.items():
+            self.kill_histogram[r] = self.kill_histogram.get(r, 0) + k
+        for b, r in o.block_r_max.items():
+            if r > self.block_r_max.get(b, 0):
+                self.block_r_max[b] = r
+        self.elapsed += o.elapsed
+        self.resume_p, self.resume_q, self.stopped = o.resume_p, o.resume_q, o.stopped
+        self.survivor_pairs = sorted(self.survivor_pairs + o.survivor_pairs)
+
+
+def validate_start(loaded: bool, p: int, q: int, opt: ScanOptions) -> int:
+    """engine.hpp:152-161."""
+    if not loaded:
+        return 6
+    if p < REGION_CROSSOVER and not opt.small_p:
+        return 2
+    if p > opt.p_limit or p == 0:
+        return 3
+    lo, hi = q_bounds(p)
+    if q < lo:
+        return 4
+    if q > hi:
+        return 5
+    return 0
+
+
+def _next_pair(p_end: int):
+    """Resume point after the last row (engine.hpp:178-187)."""
+    np_ = p_end + 1
+    return np_, (q_bounds(np_)[0] if np_ <= P_LIMIT_64BIT else 1)
+
+
+def stats_from_result(set_: SieveSet, res, with_survivors=True) -> ScanStats:
+    st = ScanStats()
+    st.pairs_tested = res.pairs_tested
+    st.survivors = res.survivors
+    st.kill_histogram = {set_.prime_at(k): int(c) for k, c in enumerate(res.hist) if c}
+    st.block_r_max = {res.block_lo + i: int(v) for i, v in enumerate(res.block_rmax) if v}
+    if with_survivors:
+        st.survivor_pairs = [(int(p), int(q)) for p, q in res.survivor_pairs]
+    return st
+
+
+def _run(set_: SieveSet, p_lo, q_start, p_hi, mode, shard, surv_cap):
+    d = set_.resident()
+    cap = surv_cap
+    while True:
+        try:
+            return d.sieve(p_lo, p_hi, mode, q_start=q_start, shard=shard, surv_cap=cap)
+        except N.CudaSieveError as e:
+            if e.code != N.ERR_CAPACITY:
+                raise
+            cap = max(2 * cap, getattr(e, "survivors", 0) + 1)
+
+
+def scan(set_: SieveSet, start, p_end: int, sink: Optional[Callable] = None,
+         opt: Optional[ScanOptions] = None, verifier: Optional[Callable] = None,
+         shard=(1, 0), surv_cap: int = 1 << 20) -> ScanStats:
+    """The reference scan() (engine.hpp:195-295) on the GPU: REGION rows
+    q_low(p) <= q <= 59p from start=(p, q) through p_end. Survivors are handed
+    to `sink` in ascending (p, q) order as ScanEvent(p, q, verifier(p, q))."""
+    opt = opt or ScanOptions()
+    p0, q0 = int(start[0]), int(start[1])
+    if set_.empty():
+        raise ScanRejected(6)
+    code = validate_start(True, p0, q0, opt)
+    if code:
+        raise ScanRejected(code)
+    if p_end > opt.p_limit:
+        raise ScanRejected(3)
+    t0 = time.perf_counter()
+    st = ScanStats(resume_p=p0, resume_q=q0)
+    if p0 <= p_end:
+        res = _run(set_, p0, q0, p_end, N.REGION, shard, surv_cap)
+        st = stats_from_result(set_, res)
+        st.resume_p, st.resume_q = _next_pair(p_end)
+    st.elapsed = time.perf_counter() - t0
+    if sink is not None:
+        for p, q in st.survivor_pairs:
+            sink(ScanEvent(p, q, verifier(p, q) if verifier else None))
+    return st
+
+
+def scan_triangle(set_: SieveSet, p_lo: int, p_hi: int, sink: Optional[Callable] = None,
+                  verifier: Optional[Callable] = None, shard=(1, 0),
+                  surv_cap: int = 1 << 20) -> ScanStats:
+    """TRIANGLE rows 1 <= q < p for p in [p_lo, p_hi] (the BASELINE configs;
+    the loop of verify_small_region, engine.hpp:613-625, over q < p)."""
+    if set_.empty():
+        raise ScanRejected(6)
+    if p_lo < 1 or p_hi >= 1 << 32:
+        raise ScanRejected(3)
+    t0 = time.perf_counter()
+    st = ScanStats(resume_p=p_lo, resume_q=1)
+    if p_lo <= p_hi:
+        res = _run(set_, p_lo, 0, p_hi, N.TRIANGLE, shard, surv_cap)
+        st = stats_from_result(set_, res)
+        st.resume_p, st.resume_q = p_hi + 1, 1
+    st.elapsed = time.perf_counter() - t0
+    if sink is not None:
+        for p, q in st.survivor_pairs:
+            sink(ScanEvent(p, q, verifier(p, q) if verifier else None))
+    return st
+
+
+def classify(set_: SieveSet, pairs) -> np.ndarray:
+    """First-killer rank per (p, q), -1 if no table rejects it (the sieve part
+    of verify_pair, engine.hpp:72-78)."""
+    return set_.resident().classify(pairs)

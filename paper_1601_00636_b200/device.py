@@ -119,7 +119,9 @@ class Device:
         res = SieveResult(int(counts[0]), surv, hist[:n], p_lo // 100, brm[:nb],
                           spq[:k] if want_survivors else np.zeros((0, 2), np.uint64))
         if rc == N.ERR_CAPACITY:
-            raise N.CudaSieveError(rc, f"{surv} survivors exceed the buffer of {cap}")
+            err = N.CudaSieveError(rc, f"{surv} survivors exceed the buffer of {cap}")
+            err.survivors = surv
+            raise err
         return res
 
     def sieve(self, p_lo, p_hi, mode=N.TRIANGLE, q_start=0, shard=(1, 0), surv_cap=1 << 20):

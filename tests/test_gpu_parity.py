@@ -1,0 +1,296 @@
+"""Parity of the B200 path (libcuboid_gpu.so through the C ABI) with the
+reference: golden fixtures made by the unmodified reference (tests/golden/),
+the C oracle (oracle/cuboid_oracle.c) on seeded inputs, and size-independent
+properties at the BASELINE sizes. Everything is integer work: the bar is
+bit-exact equality of tables, pair counts, first-killer histograms, block
+r_max and survivor lists."""
+from __future__ import annotations
+
+import hashlib
+import random
+
+import numpy as np
+import pytest
+
+from oracle import port
+from oracle import ref as refmod
+from paper_1601_00636_b200 import _native as N
+from paper_1601_00636_b200 import cuboid
+from paper_1601_00636_b200.device import Device
+from paper_1601_00636_b200.primes import default_primes, odd_primes, primes_in_range
+
+pytestmark = pytest.mark.gpu
+
+
+def sha(b: bytes) -> str:
+    return hashlib.sha256(b).hexdigest()
+
+
+@pytest.fixture(scope="module")
+def dev():
+    d = Device(0)
+    yield d
+    d.close()
+
+
+def phi_sum(lo, hi):
+    """sum of Euler phi(p) for p in [lo, hi] = TRIANGLE candidate count."""
+    n = hi + 1
+    phi = np.arange(n, dtype=np.int64)
+    for p in range(2, n):
+        if phi[p] == p:
+            phi[p::p] -= phi[p::p] // p
+    return int(phi[max(lo, 2):n].sum())
+
+
+# ---- K1: tables ---------------------------------------------------------------------
+
+@pytest.mark.parametrize("name", ["odd32", "odd64", "odd128", "odd256", "default96"])
+@pytest.mark.parametrize("alg", [N.BUILD_PRODUCTION, N.BUILD_EXHAUSTIVE])
+def test_tables_identical_to_reference(dev, golden, sets, name, alg):
+    P = sets[name]
+    tb, evals = dev.build(P, alg)
+    g = golden["tables"][name]
+    assert len(tb) == g["bytes"]
+    if sha(tb) != g["sha256"]:  # name the first differing prime
+        for k, h in enumerate(g["per_table_sha256"]):
+            o = int(dev.offsets[k])
+            assert sha(tb[o:o + (P[k] ** 2 + 7) // 8]) == h, f"table r={P[k]} differs"
+    assert sha(tb) == g["sha256"]
+    if alg == N.BUILD_EXHAUSTIVE:
+        assert evals == sum(r ** 3 for r in P)
+    else:
+        assert 0 < evals <= sum(r * (r // 2 + 1) for r in P)
+
+
+def test_single_tables_vs_oracle(dev):
+    """test_sievetable.cpp:12-56: U_11 bytes, zero tables for r <= 7, and every
+    r <= 97 (plus large ones) equal to the definition/production oracle."""
+    assert cuboid.build_table(11).bytes == bytes.fromhex("00E09F7EEDED76CF7BDEEDF6D62FFF00")
+    for r in (2, 3, 5, 7):
+        assert cuboid.build_table(r).bytes == bytes((r * r + 7) // 8)
+    for r in primes_in_range(2, 97) + [541, 1021, 4099, 9689]:
+        for alg in (N.BUILD_PRODUCTION, N.BUILD_EXHAUSTIVE) if r < 2000 else (N.BUILD_PRODUCTION,):
+            tb, _ = dev.build([r], alg)
+            assert tb == port.build_table(r), (r, alg)
+
+
+@pytest.mark.parametrize("r", [0, 1, 4, 9697, 10007])
+def test_bad_modulus(r):
+    with pytest.raises(ValueError):
+        cuboid.build_table(r)
+
+
+def test_bad_prime_lists():
+    with pytest.raises(ValueError):
+        cuboid.SieveSet.build([13, 11])
+    with pytest.raises(ValueError):
+        cuboid.SieveSet.build([11, 15])
+
+
+def test_load_download_roundtrip_and_format_errors(dev, sets):
+    P = sets["default96"]
+    tb, _ = port.build_set(P)
+    dev.load(P, tb)
+    assert dev.download() == tb
+    assert dev.killable().all()
+    bad = bytearray(tb)
+    bad[(11 * 11 + 7) // 8 - 1] |= 0x80  # padding bit of the r = 11 table
+    with pytest.raises(cuboid.FormatError):
+        cuboid.SieveSet.from_parts(P, bytes(bad))
+    with pytest.raises(cuboid.FormatError):
+        cuboid.SieveSet.from_parts(P, tb[:-1])
+    s = cuboid.SieveSet.from_parts(odd_primes(8), port.build_set(odd_primes(8))[0])
+    assert s.resident().killable().tolist() == [False, False, False, True, True, True, True, True]
+
+
+# ---- K2: sieve against the reference's own results ---------------------------------------
+
+def _check(st: cuboid.ScanStats, g, primes):
+    assert st.pairs_tested == g["pairs_tested"]
+    assert st.survivors == g["survivors"]
+    assert {str(k): v for k, v in st.kill_histogram.items()} == g["kill_histogram"]
+    assert {str(k): v for k, v in st.block_r_max.items()} == g["block_r_max"]
+    if "survivor_sha256" in g:
+        flat = ",".join(f"{p}:{q}" for p, q in st.survivor_pairs)
+        assert sha(flat.encode()) == g["survivor_sha256"]
+    if "resume" in g:
+        assert [st.resume_p, st.resume_q] == g["resume"]
+
+
+_built = {}
+
+
+def _set(sets, name):
+    if name not in _built:
+        _built.clear()  # one resident set at a time keeps device memory small
+        _built[name] = cuboid.SieveSet.build(sets[name])
+    return _built[name]
+
+
+@pytest.mark.parametrize("name", ["C1", "C3", "C5_sub", "C4", "R152", "R152_300", "R152_2000",
+                                  "R152_5000", "R153_5000tail", "W_row1", "W_1_40", "W_T300",
+                                  "R1_151"])
+def test_sieve_identical_to_reference(golden, sets, name):
+    g = golden["sieve"][name]
+    s = _set(sets, g["set"])
+    if g["mode"] == "TRIANGLE":
+        st = cuboid.scan_triangle(s, g["p_lo"], g["p_hi"])
+    else:
+        st = cuboid.scan(s, (g["p_lo"], g["q_start"]), g["p_hi"],
+                         opt=cuboid.ScanOptions(small_p=g["p_lo"] < 152))
+    _check(st, g, sets[g["set"]])
+
+
+def test_region_pins():
+    """test_engine.cpp:71-88, 199-205 and acceptance.cpp:123-144 on the default set."""
+    s = cuboid.SieveSet.build_default()
+    st = cuboid.scan(s, (152, 3), 152)
+    assert (st.pairs_tested, st.survivors, max(st.kill_histogram)) == (4247, 0, 47)
+    assert (st.resume_p, st.resume_q) == (153, cuboid.q_bounds(153)[0])
+    st = cuboid.scan(s, (152, 3), 300)
+    assert st.survivors == 0 and max(st.kill_histogram) <= 137 and len(st.block_r_max) == 3
+    st = cuboid.scan(s, (152, 3), 5000)
+    assert (st.pairs_tested, st.survivors, max(st.kill_histogram)) == (447994938, 0, 97)
+
+
+def test_scan_rejections():
+    """ScanRejected codes (engine.hpp:152-161, 195-201; test_engine.cpp:90-122)."""
+    s = cuboid.SieveSet.build_default()
+    for start, p_end, code in [((151, 3), 200, 2), ((0, 1), 10, 2), ((72796056, 10**6), 72796056, 3),
+                               ((152, 2), 200, 4), ((152, 59 * 152 + 1), 200, 5),
+                               ((152, 3), 72796056, 3)]:
+        with pytest.raises(cuboid.ScanRejected) as e:
+            cuboid.scan(s, start, p_end)
+        assert e.value.code == code, (start, p_end)
+    with pytest.raises(cuboid.ScanRejected) as e:
+        cuboid.scan(cuboid.SieveSet([], b"", [], 0), (152, 3), 200)
+    assert e.value.code == 6
+
+
+def test_empty_range():
+    s = cuboid.SieveSet.build_default()
+    st = cuboid.scan(s, (500, 4), 499)
+    assert (st.pairs_tested, st.survivors, st.kill_histogram, st.block_r_max) == (0, 0, {}, {})
+    assert (st.resume_p, st.resume_q) == (500, 4)
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_random_ranges_vs_oracle(dev, seed):
+    """Seeded row ranges, both modes, mid-row starts, several prime sets
+    (including all-zero tables that never kill and a heavy-survivor set)."""
+    rng = random.Random(seed)
+    for P in (odd_primes(32), default_primes(), [11], [11, 13], [3, 5, 7], odd_primes(200)[150:]):
+        tb, offs = port.build_set(P)
+        dev.load(P, tb)
+        for _ in range(3):
+            mode = rng.choice([N.TRIANGLE, N.REGION])
+            lo = rng.randrange(1, 4000)
+            hi = lo + rng.choice([0, 1, 7, 99, 250] if mode == N.TRIANGLE else [0, 1, 7])
+            q0 = 0
+            if mode == N.REGION and rng.random() < 0.5:
+                q0 = rng.randrange(*cuboid.q_bounds(lo))
+            o = port.sieve(tb, P, offs, lo, hi, mode, q_start=q0)
+            r = dev.sieve(lo, hi, mode, q_start=q0, surv_cap=1 << 22)
+            assert r.pairs_tested == o["pairs_tested"], (P[:3], mode, lo, hi, q0)
+            assert r.survivors == o["survivors"]
+            assert r.hist.tolist() == o["hist"].tolist()
+            assert np.array_equal(r.survivor_pairs, o["survivor_pairs"])
+            rows = np.asarray(o["row_rmax"])
+            want = {}
+            for i, v in enumerate(rows):
+                b = (lo + i) // 100
+                want[b] = max(want.get(b, 0), int(v))
+            got = {r.block_lo + i: int(v) for i, v in enumerate(r.block_rmax) if v}
+            assert got == want
+
+
+def test_heavy_survivor_compaction(dev):
+    """Weak sieve {11} (test_engine.cpp:177-197) over C1's triangle: 405,546
+    survivors, emitted in canonical ascending (p, q) order."""
+    P = [11]
+    tb, offs = port.build_set(P)
+    dev.load(P, tb)
+    o = port.sieve(tb, P, offs, 2, 2000, port.TRIANGLE)
+    r = dev.sieve(2, 2000, N.TRIANGLE, surv_cap=1 << 20)
+    assert r.survivors == o["survivors"] == 405546
+    assert np.array_equal(r.survivor_pairs, o["survivor_pairs"])
+    with pytest.raises(N.CudaSieveError) as e:
+        dev.sieve(2, 2000, N.TRIANGLE, surv_cap=1000)
+    assert e.value.code == N.ERR_CAPACITY and e.value.survivors == 405546
+
+
+@pytest.mark.skipif(not refmod.available(), reason="oracle/_ref not built")
+def test_survivors_reach_the_reference_final_check():
+    """scan() hands each survivor to verify_pair(bypass) in order (engine.hpp:272-277)."""
+    rs = refmod.RefSet.build([11])
+    s = cuboid.SieveSet.build([11])
+    events = []
+    st = cuboid.scan(s, (1, 1), 1, sink=events.append, opt=cuboid.ScanOptions(small_p=True),
+                     verifier=lambda p, q: refmod.verify_pair(rs, p, q, True)[0])
+    ref = refmod.scan(rs, 1, 1, 1, small_p=True)
+    assert [(e.p, e.q, e.verdict) for e in events] == ref.survivor_pairs
+    assert st.survivors == len(events) > 0
+
+
+# ---- multi-shard semantics (ScanStats::merge, test_engine.cpp:134-175) -----------------
+
+@pytest.mark.parametrize("G", [2, 3, 8])
+def test_block_cyclic_shards_merge_to_full(dev, golden, sets, G):
+    g = golden["sieve"]["C3"]
+    tb, _ = port.build_set(sets["odd64"])
+    dev.load(sets["odd64"], tb)
+    hist = np.zeros(64, np.uint64)
+    pairs = surv = 0
+    brm = {}
+    for k in range(G):
+        r = dev.sieve(2, 10000, N.TRIANGLE, shard=(G, k))
+        pairs += r.pairs_tested
+        surv += r.survivors
+        hist += r.hist
+        for i, v in enumerate(r.block_rmax):
+            if v:
+                assert (r.block_lo + i) % G == k  # each block lives on one shard
+                brm[r.block_lo + i] = int(v)
+    assert pairs == g["pairs_tested"] and surv == 0
+    assert {str(sets["odd64"][k]): int(c) for k, c in enumerate(hist) if c} == g["kill_histogram"]
+    assert {str(b): v for b, v in sorted(brm.items())} == g["block_r_max"]
+
+
+# ---- BASELINE full sizes: size-independent properties ------------------------------------
+
+def test_c5_full_range_properties(dev, golden, sets):
+    """C5 (10^5 < p <= 3*10^5, 256 primes, 2.43e10 pairs): pairs = sum phi(p);
+    every pair is killed or survives; 4-way block-cyclic shards merge to the
+    full result; the reference-checked 1000-row sub-range agrees."""
+    s = _set(sets, "odd256")
+    full = cuboid.scan_triangle(s, 100001, 300000)
+    assert full.pairs_tested == phi_sum(100001, 300000) == 24317097730
+    assert full.histogram_total() + full.survivors == full.pairs_tested
+    merged = cuboid.ScanStats()
+    for k in range(4):
+        merged.merge(cuboid.scan_triangle(s, 100001, 300000, shard=(4, k)))
+    assert (merged.pairs_tested, merged.survivors, merged.kill_histogram, merged.block_r_max) == \
+        (full.pairs_tested, full.survivors, full.kill_histogram, full.block_r_max)
+    sub = cuboid.scan_triangle(s, 200001, 201000)
+    _check(sub, golden["sieve"]["C5_sub"], sets["odd256"])
+
+
+def test_c4_random_subsample_classify(dev, sets):
+    """C4's seeded 10^6-pair subsample: first-killer rank of each
+    pair from the device classify path == the C oracle's rank-ordered probe."""
+    P = sets["odd128"]
+    tb, offs = port.build_set(P)
+    dev.load(P, tb)
+    rng = np.random.default_rng(20160401)
+    p = rng.integers(2, 100001, 10**6, dtype=np.uint64)
+    q = (rng.integers(0, 1 << 62, 10**6, dtype=np.uint64) % (p - 1)) + 1
+    got = dev.classify(np.stack([p, q], 1))
+    # oracle: same rank-ordered probe, vectorised over the packed bytes
+    want = np.full(len(p), -1, np.int64)
+    buf = np.frombuffer(tb, np.uint8)
+    for k, r in enumerate(P):
+        i = (p % r) * r + (q % r)
+        hit = ((buf[offs[k] + (i >> 3)] >> (i & 7).astype(np.uint8)) & 1).astype(bool)
+        want[(want < 0) & hit] = k
+    assert np.array_equal(got, want)
