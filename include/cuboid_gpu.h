@@ -157,10 +157,11 @@ int cgpu_sieve_launch_dev(cgpu_ctx* ctx, uint64_t p_lo, uint64_t q_start, uint64
  * ms[2] = both. */
 int cgpu_last_timings(cgpu_ctx* ctx, float* ms3);
 
-/* Measured INT32 throughput of `device` in thread-ops/s: ops3[0] = LOP3 chains
- * (ALU pipe), ops3[1] = IMAD chains (FMA pipe), ops3[2] = both interleaved
- * (the issue-bound ceiling). The roofline denominators of the bench. */
-int cgpu_int32_peak(int device, double* ops3);
+/* Measured INT32 throughput of `device` in thread-ops/s: ops4[0] = LOP3 chains
+ * (ALU pipe), ops4[1] = IMAD chains (FMA pipe), ops4[2] = IMAD + LOP3
+ * interleaved (3 register sources each), ops4[3] = IMAD + LOP3 with
+ * immediates (the issue-bound ceiling). The roofline denominators of the bench. */
+int cgpu_int32_peak(int device, double* ops4);
 
 /* Number of kernels the last cgpu_sieve_launch / cgpu_tables_* enqueued. */
 int cgpu_last_launch_count(cgpu_ctx* ctx, uint32_t* n);

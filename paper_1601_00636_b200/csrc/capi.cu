@@ -696,14 +696,14 @@ int cgpu_last_timings(cgpu_ctx* c, float* ms3)
 	return CGPU_OK;
 }
 
-int cgpu_int32_peak(int device, double* ops3)
+int cgpu_int32_peak(int device, double* ops4)
 {
-	if (!ops3) return set_err(CGPU_ERR_INVALID, "null argument");
+	if (!ops4) return set_err(CGPU_ERR_INVALID, "null argument");
 	int count = 0;
 	if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0)
 		return set_err(CGPU_ERR_NO_DEVICE, "no CUDA device visible: cuboid_gpu has no CPU fallback");
 	CK(cudaSetDevice(device));
-	CK(run_int_peak(device, ops3));
+	CK(run_int_peak(device, ops4));
 	return CGPU_OK;
 }
 

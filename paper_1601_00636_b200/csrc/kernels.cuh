@@ -92,7 +92,8 @@ cudaError_t launch_classify(const uint64_t* d_pq, uint64_t n, const uint8_t* d_p
                             const uint32_t* d_primes, const uint32_t* d_offsets, uint32_t nprimes,
                             int32_t* d_out, cudaStream_t s);
 
-// INT32 pipe peaks (peak.cu): out = {LOP3-only, IMAD-only, mixed} thread-ops/s.
-cudaError_t run_int_peak(int device, double out[3]);
+// INT32 pipe peaks (peak.cu), thread-ops/s: {LOP3-only, IMAD-only,
+// IMAD+LOP3 3-register, IMAD+LOP3 immediate forms}.
+cudaError_t run_int_peak(int device, double out[4]);
 
 }  // namespace cgpu

@@ -12,7 +12,9 @@ constexpr int kChains = 8;
 constexpr int kIters = 2048;
 constexpr int kPeakThreads = 256;
 
-// mode 0: LOP3 only; 1: IMAD only; 2: one IMAD + one LOP3 per step.
+// mode 0: LOP3 only; 1: IMAD only; 2: one IMAD + one LOP3 per step (3 register
+// sources each); 3: IMAD + IADD3 with immediate operands (fewer register-file
+// reads: the issue-bound ceiling of one warp instruction per clock per SMSP).
 template <int MODE>
 __global__ void __launch_bounds__(kPeakThreads) k_int_peak(uint32_t seed, uint32_t* sink)
 {
@@ -26,6 +28,11 @@ __global__ void __launch_bounds__(kPeakThreads) k_int_peak(uint32_t seed, uint32
 	for (int it = 0; it < kIters; ++it) {
 #pragma unroll
 		for (int i = 0; i < kChains; ++i) {
+			if (MODE == 3) {
+				asm volatile("mad.lo.u32 %0, %0, 0x9E3779B1, %1;" : "+r"(x[i]) : "r"(y[i]));
+				asm volatile("lop3.b32 %0, %0, %1, 0x7F4A7C15, 0x96;" : "+r"(y[i]) : "r"(x[i]));
+				continue;
+			}
 			if (MODE != 0) asm volatile("mad.lo.u32 %0, %0, %1, %2;" : "+r"(x[i]) : "r"(a), "r"(b));
 			if (MODE != 1)
 				asm volatile("lop3.b32 %0, %0, %1, %2, 0x96;" : "+r"(y[i]) : "r"(c), "r"(x[i]));
@@ -39,7 +46,7 @@ __global__ void __launch_bounds__(kPeakThreads) k_int_peak(uint32_t seed, uint32
 
 }  // namespace
 
-cudaError_t run_int_peak(int device, double out[3])
+cudaError_t run_int_peak(int device, double out[4])
 {
 	int sms = 0;
 	cudaError_t e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
@@ -51,10 +58,11 @@ cudaError_t run_int_peak(int device, double out[3])
 	cudaEventCreate(&t1);
 	const int grid = sms * 8;  // 8 CTAs x 8 warps = 64 warps per SM
 	const double threads = static_cast<double>(grid) * kPeakThreads;
-	void (*fns[3])(uint32_t, uint32_t*) = {k_int_peak<0>, k_int_peak<1>, k_int_peak<2>};
-	const double ops_per_thread[3] = {1.0 * kIters * kChains, 1.0 * kIters * kChains,
-	                                  2.0 * kIters * kChains};
-	for (int m = 0; m < 3 && e == cudaSuccess; ++m) {
+	void (*fns[4])(uint32_t, uint32_t*) = {k_int_peak<0>, k_int_peak<1>, k_int_peak<2>,
+	                                       k_int_peak<3>};
+	const double ops_per_thread[4] = {1.0 * kIters * kChains, 1.0 * kIters * kChains,
+	                                  2.0 * kIters * kChains, 2.0 * kIters * kChains};
+	for (int m = 0; m < 4 && e == cudaSuccess; ++m) {
 		float best = 1e30f;
 		for (int rep = 0; rep < 5; ++rep) {
 			cudaEventRecord(t0);

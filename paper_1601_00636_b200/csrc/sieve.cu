@@ -281,7 +281,7 @@ __global__ void __launch_bounds__(kSieveThreads) k_sieve(const SieveArgs a)
 					const uint32_t k = alive & M;
 					if (k) {
 						atomicAdd(&s_hist[j], static_cast<unsigned long long>(__popc(k)));
-						deep_max = j + 1;
+						deep_max = max(deep_max, j + 1);
 						alive ^= k;
 						if (!alive) break;
 					}
