@@ -1,0 +1,117 @@
+"""Multi-GPU sieve: block-cyclic p-row partitioning + cross-rank reduction.
+
+One process per GPU (torch.distributed, NCCL over NVLink/NVSwitch). Rows p are
+grouped in the reference's p/100 blocks (the ScanStats::block_r_max key,
+engine.hpp:229-236); rank g of G owns the blocks b with b % G == g, which
+balances the linearly growing row lengths and keeps every block on one rank.
+Each rank sieves its blocks into device buffers (cgpu_sieve_launch_dev) and
+the ranks then combine exactly as ScanStats::merge does (engine.hpp:121-134):
+
+    sum  : pairs_tested, survivors, first-killer histogram   (all_reduce SUM)
+    max  : block r_max (0 marks blocks a rank does not own)    (all_reduce MAX)
+    cat  : survivor lists, then sorted to canonical (p, q)     (all_gather)
+
+The same reduction code runs on CPU tensors over gloo (tests) and on CUDA
+tensors over NCCL (the product path and bench.py).
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _native as N
+
+
+def owned_blocks(p_lo: int, p_hi: int, G: int, g: int) -> list[int]:
+    """Blocks b = p // 100 in [p_lo // 100, p_hi // 100] with b % G == g."""
+    if p_hi < p_lo:
+        return []
+    b0, b1 = p_lo // 100, p_hi // 100
+    first = b0 + ((g - b0) % G)
+    return list(range(first, b1 + 1, G))
+
+
+def owned_rows(p_lo: int, p_hi: int, G: int, g: int):
+    """(lo, hi) row intervals of rank g's shard, clipped to [p_lo, p_hi]."""
+    return [(max(p_lo, 100 * b), min(p_hi, 100 * b + 99)) for b in owned_blocks(p_lo, p_hi, G, g)]
+
+
+def reduce_results(acc, brm, group=None):
+    """In place: acc = [pairs, survivors, hist...] (int64) summed over ranks,
+    brm (int32 block r_max, 0 = not owned) max-reduced."""
+    import torch.distributed as dist
+    dist.all_reduce(acc, op=dist.ReduceOp.SUM, group=group)
+    dist.all_reduce(brm, op=dist.ReduceOp.MAX, group=group)
+    return acc, brm
+
+
+def gather_survivors(keys, count: int, group=None):
+    """All-gather variable-length survivor lists. keys: int64 tensor holding
+    this rank's `count` survivors as (p << 32) | q (any order). Returns a
+    sorted numpy uint64 array of (p, q) rows -- the canonical order of the
+    reference's sink (engine.hpp:272-277)."""
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    n = torch.tensor([count], dtype=torch.int64, device=keys.device)
+    counts = [torch.zeros_like(n) for _ in range(world)]
+    dist.all_gather(counts, n, group=group)
+    counts = [int(c.item()) for c in counts]
+    m = max(counts)
+    if m == 0:
+        return np.zeros((0, 2), np.uint64)
+    pad = torch.zeros(m, dtype=torch.int64, device=keys.device)
+    pad[:count] = keys[:count]
+    parts = [torch.zeros_like(pad) for _ in range(world)]
+    dist.all_gather(parts, pad, group=group)
+    allk = np.concatenate([p[:c].cpu().numpy() for p, c in zip(parts, counts)]).astype(np.uint64)
+    allk.sort()
+    return np.stack([allk >> np.uint64(32), allk & np.uint64(0xFFFFFFFF)], 1)
+
+
+class ShardedSieve:
+    """The product multi-GPU path: this rank's shard on its own GPU, results
+    reduced over the default process group (NCCL)."""
+
+    def __init__(self, dev, primes, surv_cap: int = 1 << 20):
+        import torch
+        self.dev = dev
+        self.primes = list(primes)
+        self.surv_cap = surv_cap
+        self.cuda = torch.device("cuda", dev.device)
+        self.acc = torch.zeros(2 + len(self.primes), dtype=torch.int64, device=self.cuda)
+        self.surv = torch.zeros(max(surv_cap, 1), dtype=torch.int64, device=self.cuda)
+        self.brm = None
+
+    def launch(self, p_lo, p_hi, mode=N.TRIANGLE, q_start=0):
+        import torch
+        import torch.distributed as dist
+        G = dist.get_world_size() if dist.is_initialized() else 1
+        g = dist.get_rank() if dist.is_initialized() else 0
+        nb = p_hi // 100 - p_lo // 100 + 1 if p_hi >= p_lo else 0
+        if self.brm is None or self.brm.numel() < max(nb, 1):
+            self.brm = torch.zeros(max(nb, 1), dtype=torch.int32, device=self.cuda)
+        self.nb = nb
+        N.check(N.lib().cgpu_sieve_launch_dev(
+            self.dev._ctx, int(p_lo), int(q_start), int(p_hi), int(mode), G, g,
+            C.c_void_p(self.acc.data_ptr()), C.c_void_p(self.acc.data_ptr() + 16),
+            C.c_void_p(self.brm.data_ptr()), max(nb, 1), C.c_void_p(self.surv.data_ptr()),
+            self.surv_cap))
+
+    def reduce(self):
+        """Reduce over ranks; returns (pairs, survivors, hist, block_rmax, survivor_pairs)."""
+        import torch.distributed as dist
+        self.dev.synchronize()  # the context stream may differ from torch's current stream
+        local_surv = int(self.acc[1].item())
+        if local_surv > self.surv_cap:
+            raise N.CudaSieveError(N.ERR_CAPACITY, f"{local_surv} survivors exceed {self.surv_cap}")
+        keys = self.surv
+        if dist.is_initialized() and dist.get_world_size() > 1:
+            reduce_results(self.acc, self.brm[:max(self.nb, 1)])
+            pairs = gather_survivors(keys, local_surv)
+        else:
+            k = np.sort(keys[:local_surv].cpu().numpy().astype(np.uint64))
+            pairs = np.stack([k >> np.uint64(32), k & np.uint64(0xFFFFFFFF)], 1)
+        a = self.acc.cpu().numpy()
+        return int(a[0]), int(a[1]), a[2:].copy(), self.brm[:self.nb].cpu().numpy(), pairs

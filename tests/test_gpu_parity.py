@@ -294,3 +294,18 @@ def test_c4_random_subsample_classify(dev, sets):
         hit = ((buf[offs[k] + (i >> 3)] >> (i & 7).astype(np.uint8)) & 1).astype(bool)
         want[(want < 0) & hit] = k
     assert np.array_equal(got, want)
+
+
+def test_sharded_sieve_single_rank(dev):
+    """parallel.ShardedSieve (the multi-GPU product path) at world size 1."""
+    from paper_1601_00636_b200.parallel import ShardedSieve
+    P = [11, 13]
+    tb, offs = port.build_set(P)
+    dev.load(P, tb)
+    s = ShardedSieve(dev, P)
+    s.launch(2, 700)
+    pairs, surv, hist, brm, sp = s.reduce()
+    o = port.sieve(tb, P, offs, 2, 700, port.TRIANGLE)
+    assert (pairs, surv) == (o["pairs_tested"], o["survivors"])
+    assert hist.tolist() == o["hist"].astype(np.int64).tolist()
+    assert np.array_equal(sp, o["survivor_pairs"])

@@ -1,0 +1,115 @@
+"""Host-side multi-rank logic on the CPU (gloo, world_size 2 and 3): the
+block-cyclic partitioner covers every row exactly once, and the cross-rank
+reduction + survivor gather of paper_1601_00636_b200.parallel turns per-rank
+shard results into exactly the single-process result (ScanStats::merge,
+engine.hpp:121-134; split/merge tests test_engine.cpp:134-175). Per-rank shard
+results come from the C oracle here, laid out exactly as the device writes
+them (cgpu_sieve_launch_dev)."""
+from __future__ import annotations
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle import port
+from paper_1601_00636_b200 import parallel
+from paper_1601_00636_b200.primes import default_primes, odd_primes
+
+
+def test_partition_covers_rows_once():
+    for (lo, hi) in [(2, 10000), (152, 5000), (100001, 300000), (1, 99), (250, 251), (7, 6)]:
+        for G in (1, 2, 3, 4, 8):
+            seen = []
+            for g in range(G):
+                for b in parallel.owned_blocks(lo, hi, G, g):
+                    assert b % G == g
+                for (a, z) in parallel.owned_rows(lo, hi, G, g):
+                    seen.extend(range(a, z + 1))
+            assert sorted(seen) == list(range(lo, hi + 1))
+
+
+def test_partition_balances_triangle_work():
+    """Block-cyclic over 8 ranks keeps C5's per-rank pair counts within 1%."""
+    work = []
+    for g in range(8):
+        work.append(sum((a + z) * (z - a + 1) // 2 for a, z in parallel.owned_rows(100001, 300000, 8, g)))
+    assert max(work) / min(work) < 1.01
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _shard_result(tb, P, offs, lo, hi, mode, G, g, q_start):
+    """Oracle shard result in the device output layout."""
+    n = len(P)
+    acc = np.zeros(2 + n, np.int64)
+    nb = hi // 100 - lo // 100 + 1
+    brm = np.zeros(nb, np.int32)
+    keys = []
+    for (a, z) in parallel.owned_rows(lo, hi, G, g):
+        o = port.sieve(tb, P, offs, a, z, mode, q_start=q_start if a == lo else 0)
+        acc[0] += o["pairs_tested"]
+        acc[1] += o["survivors"]
+        acc[2:] += o["hist"].astype(np.int64)
+        for i, v in enumerate(o["row_rmax"]):
+            b = (a + i) // 100 - lo // 100
+            brm[b] = max(brm[b], int(v))
+        keys.extend((int(p) << 32) | int(q) for p, q in o["survivor_pairs"])
+    rng = np.random.default_rng(g)
+    keys = np.array(keys, np.int64)
+    rng.shuffle(keys)  # device survivors come out unordered
+    return acc, brm, keys
+
+
+def _worker(rank, world, port_, case, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port_)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    P, lo, hi, mode, q_start = case
+    tb, offs = port.build_set(P)
+    acc, brm, keys = _shard_result(tb, P, offs, lo, hi, mode, world, rank, q_start)
+    acc_t, brm_t = torch.from_numpy(acc), torch.from_numpy(brm)
+    keys_t = torch.zeros(max(len(keys), 1), dtype=torch.int64)
+    keys_t[:len(keys)] = torch.from_numpy(keys)
+    parallel.reduce_results(acc_t, brm_t)
+    surv = parallel.gather_survivors(keys_t, len(keys))
+    out[rank] = (acc_t.numpy().tolist(), brm_t.numpy().tolist(), surv.tolist())
+    dist.destroy_process_group()
+
+
+CASES = [
+    (odd_primes(32), 2, 2000, port.TRIANGLE, 0),        # C1
+    ([11], 2, 700, port.TRIANGLE, 0),                   # weak sieve: heavy survivor gather
+    (default_primes(), 152, 1400, port.REGION, 3),      # reference region
+    ([11, 13], 160, 555, port.REGION, 777),             # mid-row start, survivors
+]
+
+
+@pytest.mark.parametrize("world,case", [(2, 0), (2, 1), (2, 2), (3, 3)])
+def test_gloo_reduction_equals_single_process(world, case):
+    P, lo, hi, mode, q_start = CASES[case]
+    tb, offs = port.build_set(P)
+    full = port.sieve(tb, P, offs, lo, hi, mode, q_start=q_start)
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_worker, args=(world, _free_port(), CASES[case], out), nprocs=world, join=True)
+    want_brm = {}
+    for i, v in enumerate(full["row_rmax"]):
+        b = (lo + i) // 100
+        want_brm[b] = max(want_brm.get(b, 0), int(v))
+    for r in range(world):
+        acc, brm, surv = out[r]
+        assert acc[0] == full["pairs_tested"] and acc[1] == full["survivors"]
+        assert acc[2:] == full["hist"].astype(np.int64).tolist()
+        assert {lo // 100 + i: v for i, v in enumerate(brm)} == want_brm
+        assert surv == full["survivor_pairs"].tolist()
