@@ -9,7 +9,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libcuboid_gpu.so")
+LIB_PATH = os.environ.get("CUBOID_GPU_LIB", os.path.join(HERE, "libcuboid_gpu.so"))
 
 # status codes (cuboid_gpu.h)
 OK = 0

@@ -4,6 +4,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -137,11 +138,13 @@ struct cgpu_ctx {
 	uint32_t reg_r[kMaxReg] = {}, reg_m[kMaxReg] = {}, reg_base[kMaxReg] = {}, reg_delta[kMaxReg] = {};
 	int grid[kMaxReg + 1] = {};
 
+	uint32_t row_cost = kDefaultRowCost;
 	DevBuf<uint2> fprimes;
 	uint32_t n_fprimes = 0;
 
 	// sieve buffers
-	DevBuf<unsigned long long> hist, counters, surv, prefix;
+	DevBuf<unsigned long long> hist, counters, surv, prefix, chunk_off;
+	DevBuf<uint32_t> tickets;
 	DevBuf<uint32_t> d_probe_rank;
 	DevBuf<uint32_t> block_rmax;
 	bool launched = false, results_internal = false, timed = false;
@@ -199,6 +202,7 @@ int cgpu_create(int device, void* stream, cgpu_ctx** out)
 		c->own_stream = true;
 	}
 	cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device);
+	if (const char* rc = std::getenv("CUBOID_ROW_COST")) c->row_cost = static_cast<uint32_t>(std::atoi(rc));
 	for (auto& e : c->ev) cudaEventCreate(&e);
 	// trial-division primes below 2^16 (covers sqrt of any p < 2^32)
 	std::vector<uint2> fp;
@@ -557,12 +561,14 @@ int enqueue_sieve(cgpu_ctx* c, uint64_t p_lo, uint64_t q_start, uint64_t p_hi, i
 	}
 	a.fprimes = c->fprimes.p;
 	a.n_fprimes = c->n_fprimes;
+	a.row_cost = c->row_cost;
 	a.p_lo = p_lo;
 	a.p_hi = p_hi;
 	a.q_start = q_start;
 	a.mode = mode;
 	a.G = G;
 	a.hist = d_hist;
+	a.nprimes = static_cast<uint32_t>(c->primes.size());
 	a.probe_rank = c->d_probe_rank.p;
 	a.counters = d_counts;
 	a.block_rmax = d_block_rmax;
@@ -575,13 +581,19 @@ int enqueue_sieve(cgpu_ctx* c, uint64_t p_lo, uint64_t q_start, uint64_t p_hi, i
 		const uint64_t blk_hi = p_hi / 100;
 		const uint64_t first = blk_lo + ((g + G - blk_lo % G) % G);
 		const uint64_t owned = first <= blk_hi ? (blk_hi - first) / G + 1 : 0;
-		CK(c->prefix.ensure(static_cast<size_t>(std::min<uint64_t>(owned, kBlocksPerLaunch)) * 100 + 1));
+		const size_t max_slots = static_cast<size_t>(std::min<uint64_t>(owned, kBlocksPerLaunch)) * 100;
+		CK(c->prefix.ensure(max_slots + 1));
+		CK(c->chunk_off.ensure(plan_chunks(static_cast<uint32_t>(max_slots)) + 1));
+		CK(c->tickets.ensure(2));
+		CK(cudaMemsetAsync(c->tickets.p, 0, 8, c->stream));
+		a.prefix = c->prefix.p;
+		a.chunk_off = c->chunk_off.p;
+		a.tickets = c->tickets.p;
 		for (uint64_t ob = 0; ob < owned; ob += kBlocksPerLaunch) {
 			const uint64_t nb = std::min<uint64_t>(kBlocksPerLaunch, owned - ob);
 			a.blk0 = first + ob * G;
 			a.n_slots = static_cast<uint32_t>(nb * 100);
-			a.prefix = c->prefix.p;
-			CK(launch_plan(a, c->prefix.p, c->stream));
+			CK(launch_plan(a, c->stream));
 			if (!ev1) CK(cudaEventRecord(c->ev[1], c->stream));  // sieve time excludes the first plan
 			ev1 = true;
 			CK(launch_sieve(a, c->grid[c->nreg], c->stream));

@@ -50,9 +50,16 @@ constexpr uint32_t kDeriveThreads = 256;
 // ---- K2: sieve ---------------------------------------------------------------
 
 constexpr int kSieveThreads = 256;
+#ifndef CGPU_SIEVE_MIN_BLOCKS
+#define CGPU_SIEVE_MIN_BLOCKS 3
+#endif
+constexpr int kSieveMinBlocks = CGPU_SIEVE_MIN_BLOCKS;  // CTAs per SM the register budget targets
+constexpr uint32_t kDefaultRowCost = 400;                 // window-equivalents per row setup
 constexpr int kSieveWarps = kSieveThreads / 32;
 constexpr int kMaxReg = 8;      // leading probes held in registers (r <= 31)
 constexpr int kMaxFactors = 9;  // distinct prime factors of p < 2^32
+constexpr int kQueue = 64;      // per-warp deep-probe work queue entries
+constexpr uint32_t kPlanChunk = 1024;  // row slots per plan CTA
 
 struct SieveArgs {
 	const uint32_t* ext;          // row-extended tables
@@ -68,9 +75,14 @@ struct SieveArgs {
 	uint32_t G;
 	uint64_t blk0;                // first owned block of this launch
 	uint32_t n_slots;
-	const unsigned long long* prefix;  // [n_slots + 1] windows before slot
+	uint32_t row_cost;            // load-balance charge per row (window-equivalents)
+	// work units before slot s = prefix[s] + chunk_off[s / kPlanChunk]
+	unsigned long long* prefix;        // [n_slots + 1] (chunk-local exclusive scan)
+	unsigned long long* chunk_off;     // [n_chunks + 1] (exclusive scan of chunk totals)
+	uint32_t* tickets;                 // [2] last-CTA tickets (plan, sieve), zeroed per launch
 	// outputs
 	unsigned long long* hist;          // [n primes] first-killer counts by rank
+	uint32_t nprimes;
 	const uint32_t* probe_rank;        // [np] rank of probe j
 	unsigned long long* counters;      // [0] pairs_tested, [1] survivors
 	uint32_t* block_rmax;              // [p/100 - blk_lo]
@@ -79,10 +91,11 @@ struct SieveArgs {
 	unsigned long long surv_cap;
 };
 
-cudaError_t launch_plan(const SieveArgs& a, unsigned long long* d_prefix, cudaStream_t s);
+cudaError_t launch_plan(const SieveArgs& a, cudaStream_t s);
 cudaError_t launch_sieve(const SieveArgs& a, int grid, cudaStream_t s);
 int sieve_grid(int device, int nreg, size_t smem_bytes);
 size_t sieve_smem_bytes(uint32_t np);
+__host__ __device__ inline uint32_t plan_chunks(uint32_t n_slots) { return (n_slots + kPlanChunk - 1) / kPlanChunk; }
 
 cudaError_t launch_init_blocks(uint32_t* d_block_rmax, uint64_t nblocks, uint64_t blk_lo,
                                uint32_t G, uint32_t g, cudaStream_t s);

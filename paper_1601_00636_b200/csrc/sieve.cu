@@ -6,18 +6,24 @@
 //   * candidates: q in the row bounds, q != p, gcd(p, q) == 1 (engine.hpp:258);
 //   * probes in rank order, first set bit u_r(p mod r, q mod r) kills
 //     (engine.hpp:261-269); the first killer is histogrammed by rank;
+//   * every candidate is killed or survives, so pairs_tested = sum(hist) +
+//     survivors (engine.hpp:259-277) -- the kernel never counts pairs apart;
 //   * survivors are emitted as (p << 32) | q and sorted on the host;
 //   * per p/100 block, the largest killing prime (1 if none) (:229-236, 271).
 //
-// Design: bit-sliced. One thread owns a 32-wide window of
+// Design: bit-sliced. One lane owns a 32-wide window of
 // consecutive q in one row p; a probe for prime r is ONE funnel shift of two
 // words of the row-extended table (row p mod r, starting at bit q0 mod r),
-// so a single probe answers 32 pairs. Warps own contiguous slices of the
-// linearised (row, window) space, so each warp does its per-row setup (trial
-// division of p, per-prime row bases) once per row and then streams windows.
-// The leading probe primes below 32 live entirely in registers (two words
-// per row); deeper probes read the ext rows through L1. Tables that never
-// kill (all-zero, e.g. r = 3, 5, 7) are not probed -- identical results.
+// so one probe answers 32 pairs. Warps own contiguous slices of the
+// linearised (row, window) space (k_plan balances them). Per row, a warp
+// trial-divides p once; coprimality is then one periodic bit pattern per odd
+// prime factor (the loop is specialised on the factor count, so no predicated
+// dead slots), plus a constant mask for f = 2. The leading probe primes
+// (r <= 31) live entirely in registers (two words per row). Windows still
+// alive after them (a few percent) are pushed to a per-warp queue in shared
+// memory and probed against the deep tables 32 at a time, one per lane, so
+// the rare deep probes run at full SIMD width. Tables that never kill
+// (all-zero, e.g. r = 3, 5, 7) are not probed -- identical results.
 
 #include "../../include/cuboid_gpu.h"
 #include "common.cuh"
@@ -65,6 +71,9 @@ __device__ __forceinline__ RowBounds slot_row(const SieveArgs& a, uint32_t s)
 		b.qlo = q_low_dev(b.p);
 		b.qhi = 59 * b.p;
 		if (b.p == a.p_lo && a.q_start) b.qlo = a.q_start;
+		// q == p is skipped (engine.hpp:258); for p > 1 the coprimality mask
+		// removes it, for p = 1 (q_low = 1) start the row at q = 2
+		if (b.p == 1 && b.qlo == 1) b.qlo = 2;
 	}
 	return b;
 }
@@ -75,126 +84,351 @@ __device__ __forceinline__ uint64_t row_windows(const RowBounds& b)
 }
 
 // Work units of a row for load balancing: its 32-q windows plus a fixed
-// charge for the per-row setup (trial division of p, per-prime row bases),
-// measured at ~150 window-equivalents. Without it the warps that own the
-// many short rows at small p straggle (C4: one SM busy 5x longer than the rest).
-constexpr uint32_t kRowCost = 160;
-
-__device__ __forceinline__ uint64_t row_units(const RowBounds& b)
+// charge a.row_cost for the per-row setup (trial division of p, per-prime row
+// bases, the row-end queue drain). Without it the warps that own the many
+// short rows at small p straggle (C4: one SM busy 5x longer than the rest).
+__device__ __forceinline__ uint64_t row_units(const SieveArgs& a, const RowBounds& b)
 {
 	const uint64_t w = row_windows(b);
-	return w ? w + kRowCost : 0;
+	return w ? w + a.row_cost : 0;
 }
 
-// Plan: exclusive prefix of windows over row slots (one CTA).
-__global__ void __launch_bounds__(1024) k_plan(const SieveArgs a, unsigned long long* prefix)
+__device__ __forceinline__ unsigned long long slot_prefix(const SieveArgs& a, uint32_t s)
 {
-	__shared__ unsigned long long s_part[1024];
-	const uint32_t n = a.n_slots;
-	const uint32_t per = (n + blockDim.x - 1) / blockDim.x;
-	const uint32_t s0 = threadIdx.x * per;
-	const uint32_t s1 = min(n, s0 + per);
-	unsigned long long sum = 0;
-	for (uint32_t s = s0; s < s1; ++s) sum += row_units(slot_row(a, s));
-	s_part[threadIdx.x] = sum;
+	return a.prefix[s] + a.chunk_off[s / kPlanChunk];
+}
+
+// Block-wide exclusive scan of one value per thread (blockDim.x == 1024).
+__device__ __forceinline__ unsigned long long block_excl_scan(unsigned long long v,
+                                                              unsigned long long* s_warp,
+                                                              unsigned long long& total)
+{
+	const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+	unsigned long long x = v;
+#pragma unroll
+	for (int d = 1; d < 32; d <<= 1) {
+		const unsigned long long y = __shfl_up_sync(kFull, x, d);
+		if (lane >= d) x += y;
+	}
+	if (lane == 31) s_warp[wid] = x;
 	__syncthreads();
-	for (uint32_t off = 1; off < blockDim.x; off <<= 1) {
-		const unsigned long long v = threadIdx.x >= off ? s_part[threadIdx.x - off] : 0;
-		__syncthreads();
-		s_part[threadIdx.x] += v;
-		__syncthreads();
+	if (wid == 0) {
+		unsigned long long y = s_warp[lane];
+#pragma unroll
+		for (int d = 1; d < 32; d <<= 1) {
+			const unsigned long long z = __shfl_up_sync(kFull, y, d);
+			if (lane >= d) y += z;
+		}
+		s_warp[lane] = y;  // inclusive over warps
 	}
-	unsigned long long run = s_part[threadIdx.x] - sum;
-	for (uint32_t s = s0; s < s1; ++s) {
-		prefix[s] = run;
-		run += row_units(slot_row(a, s));
+	__syncthreads();
+	total = s_warp[31];
+	return x - v + (wid ? s_warp[wid - 1] : 0);
+}
+
+// Plan: per row slot, the work units before it. Each CTA scans kPlanChunk
+// slots; the last CTA to finish scans the chunk totals.
+__global__ void __launch_bounds__(kPlanChunk) k_plan(const SieveArgs a)
+{
+	__shared__ unsigned long long s_warp[32];
+	__shared__ bool s_last;
+	const uint32_t n = a.n_slots;
+	const uint32_t s = blockIdx.x * kPlanChunk + threadIdx.x;
+	const unsigned long long u = s < n ? row_units(a, slot_row(a, s)) : 0;
+	unsigned long long total;
+	const unsigned long long ex = block_excl_scan(u, s_warp, total);
+	if (s < n) a.prefix[s] = ex;
+	if (s == n - 1) a.prefix[n] = (n % kPlanChunk) ? ex + u : 0;
+	if (threadIdx.x == 0) a.chunk_off[blockIdx.x] = total;
+	__threadfence();
+	__syncthreads();
+	if (threadIdx.x == 0) s_last = atomicAdd(&a.tickets[0], 1u) == gridDim.x - 1;
+	__syncthreads();
+	if (!s_last) return;
+	__threadfence();
+	const uint32_t nc = gridDim.x;  // <= kPlanChunk (kMaxSlots / kPlanChunk)
+	const unsigned long long v =
+	    threadIdx.x < nc ? *reinterpret_cast<volatile unsigned long long*>(a.chunk_off + threadIdx.x) : 0;
+	__syncthreads();
+	const unsigned long long cex = block_excl_scan(v, s_warp, total);
+	if (threadIdx.x < nc) a.chunk_off[threadIdx.x] = cex;
+	if (threadIdx.x == 0) {
+		a.chunk_off[nc] = total;
+		a.tickets[0] = 0;  // ready for the next launch on this stream
 	}
-	if (threadIdx.x == blockDim.x - 1) prefix[n] = s_part[blockDim.x - 1];
 }
 
 __device__ __forceinline__ uint32_t warp_sum(uint32_t v)
 {
-	for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
-	return v;
+	return __reduce_add_sync(kFull, v);
+}
+
+// Per-warp first-kill counters in shared memory are 32-bit; a wrap is carried
+// to the 64-bit global histogram by the lane that caused it (lane 0 only).
+__device__ __forceinline__ void hist_add(const SieveArgs& a, uint32_t* h, uint32_t j, uint32_t c)
+{
+	const uint32_t old = h[j];
+	const uint32_t nw = old + c;
+	h[j] = nw;
+	if (nw < old) atomicAdd(&a.hist[__ldg(a.probe_rank + j)], 1ull << 32);
+}
+
+struct WarpSmem {
+	uint4* desc;     // [np] per deep probe: {row word base, r, m, -} for the current row
+	uint2* queue;    // [kQueue] windows alive after the register probes: {q0, alive}
+	uint32_t* hist;  // [np] first-kill counts of this warp
+};
+
+// Warp-aggregated survivor output: one atomic per warp.
+__device__ __forceinline__ void emit_survivors(const SieveArgs& a, uint32_t lane, uint32_t p,
+                                               uint32_t q0, uint32_t alive)
+{
+	if (!__any_sync(kFull, alive)) return;
+	const uint32_t n = __popc(alive);
+	uint32_t x = n;
+#pragma unroll
+	for (int d = 1; d < 32; d <<= 1) {
+		const uint32_t y = __shfl_up_sync(kFull, x, d);
+		if (lane >= d) x += y;
+	}
+	const uint32_t total = __shfl_sync(kFull, x, 31);
+	unsigned long long base = 0;
+	if (lane == 31) base = atomicAdd(&a.counters[1], static_cast<unsigned long long>(total));
+	base = __shfl_sync(kFull, base, 31) + (x - n);
+	while (alive) {
+		const uint32_t bit = __ffs(alive) - 1;
+		alive &= alive - 1;
+		if (base < a.surv_cap) a.surv[base] = (static_cast<unsigned long long>(p) << 32) | (q0 + bit);
+		++base;
+	}
+}
+
+// Probes queue entries [base, base + n) (n <= 32, one per lane) against the
+// deep tables in rank order; the lanes step through the probes together and
+// leave as soon as every entry is dead. kmax = 1 + deepest killing probe.
+template <int NREG>
+__device__ __forceinline__ void drain(const SieveArgs& a, const WarpSmem& w, uint32_t lane, uint32_t base,
+                                   uint32_t n, uint32_t p, uint32_t& kmax)
+{
+	uint32_t q0 = 0, alive = 0;
+	if (lane < n) {
+		const uint2 e = w.queue[base + lane];
+		q0 = e.x;
+		alive = e.y;
+	}
+	for (uint32_t j = NREG; j < a.np; ++j) {
+		if (!__any_sync(kFull, alive)) break;
+		uint32_t c = 0;
+		if (alive) {
+			const uint4 d = w.desc[j];
+			const uint32_t b = mod_full(q0, d.y, d.z);
+			const uint32_t* wp = a.ext + d.x + (b >> 5);
+			const uint32_t M = __funnelshift_r(__ldg(wp), __ldg(wp + 1), b);
+			const uint32_t k = alive & M;
+			alive ^= k;
+			c = __popc(k);
+		}
+		c = warp_sum(c);
+		if (c) {
+			kmax = max(kmax, j + 1);
+			if (lane == 0) hist_add(a, w.hist, j, c);
+		}
+	}
+	emit_survivors(a, lane, p, q0, alive);
+}
+
+// Row context handed to the specialised window loop.
+struct RowCtx {
+	uint32_t p, qlo, w0, w1, wlast, tail, even;
+	uint32_t nf;
+	uint32_t fac[kMaxFactors];  // odd prime factors of p that can divide some q of the row
+};
+
+// The window loop of one row segment, specialised on the number of odd prime
+// factors NF so the coprimality masks cost exactly NF x 4 instructions.
+// Returns 1 + the deepest probe that killed in this segment (0: none).
+template <int NREG, int NF>
+__device__ __forceinline__ uint32_t row_loop(const SieveArgs& a, const WarpSmem& w, uint32_t lane,
+                                             const RowCtx& rc)
+{
+	uint32_t cnt[NREG > 0 ? NREG : 1];
+#pragma unroll
+	for (int j = 0; j < NREG; ++j) cnt[j] = 0;
+	uint32_t kmax = 0;
+	const uint32_t q0_first = rc.qlo + 32 * (rc.w0 + lane);
+	uint32_t fo[NF > 0 ? NF : 1], fd[NF > 0 ? NF : 1], fpat[NF > 0 ? NF : 1], ff[NF > 0 ? NF : 1];
+#pragma unroll
+	for (int k = 0; k < NF; ++k) {
+		const uint32_t f = rc.fac[k];
+		const uint32_t b = q0_first % f;
+		ff[k] = f;
+		fo[k] = b ? f - b : 0;
+		fd[k] = kStepQ % f;
+		fpat[k] = period_mask(f);
+	}
+	uint32_t rw0[NREG > 0 ? NREG : 1], rw1[NREG > 0 ? NREG : 1], rb[NREG > 0 ? NREG : 1];
+#pragma unroll
+	for (int j = 0; j < NREG; ++j) {
+		const uint32_t r = a.reg_r[j], m = a.reg_m[j];
+		const uint32_t row = a.reg_base[j] + mod_full(rc.p, r, m) * 2;  // S = 2 for r <= 31
+		rw0[j] = __ldg(a.ext + row);
+		rw1[j] = __ldg(a.ext + row + 1);
+		rb[j] = mod_full(q0_first, r, m);
+	}
+	const uint32_t lt = (1u << lane) - 1;
+	uint32_t qn = 0;  // queued windows
+	const uint32_t n_iter = (rc.w1 - rc.w0 + 31) / 32;
+	for (uint32_t it = 0; it < n_iter; ++it) {
+		const uint32_t wi = rc.w0 + lane + 32 * it;
+		const uint32_t q0 = rc.qlo + 32 * wi;
+		uint32_t alive = wi < rc.w1 ? (wi < rc.wlast ? kFull : rc.tail) : 0u;
+		uint32_t nonc = rc.even;
+#pragma unroll
+		for (int k = 0; k < NF; ++k) {
+			nonc |= shl_clamp(fpat[k], fo[k]);
+			const uint32_t t = fo[k] - fd[k];
+			fo[k] = min(t, t + ff[k]);
+		}
+		alive &= ~nonc;
+#pragma unroll
+		for (int j = 0; j < NREG; ++j) {
+			const uint32_t M = __funnelshift_r(rw0[j], rw1[j], rb[j]);
+			const uint32_t k = alive & M;
+			cnt[j] += __popc(k);
+			alive ^= k;
+			const uint32_t t = rb[j] + a.reg_delta[j];
+			rb[j] = min(t, t - a.reg_r[j]);
+		}
+		const uint32_t m = __ballot_sync(kFull, alive != 0);
+		if (m) {
+			if (alive) w.queue[qn + __popc(m & lt)] = make_uint2(q0, alive);
+			qn += __popc(m);
+			if (qn >= 32) {
+				__syncwarp();
+				qn -= 32;
+				drain<NREG>(a, w, lane, qn, 32, rc.p, kmax);
+				__syncwarp();
+			}
+		}
+	}
+	if (qn) {
+		__syncwarp();
+		drain<NREG>(a, w, lane, 0, qn, rc.p, kmax);
+		__syncwarp();
+	}
+	// register-probe counts of this segment (per-row sums are < 2^32: 59p < 2^32)
+#pragma unroll
+	for (int j = 0; j < NREG; ++j) {
+		const uint32_t s = warp_sum(cnt[j]);
+		if (s) {
+			kmax = max(kmax, static_cast<uint32_t>(j + 1));
+			if (lane == 0) hist_add(a, w.hist, j, s);
+		}
+	}
+	return kmax;
 }
 
 template <int NREG>
-__global__ void __launch_bounds__(kSieveThreads) k_sieve(const SieveArgs a)
+__device__ __forceinline__ uint32_t dispatch_row(const SieveArgs& a, const WarpSmem& w, uint32_t lane,
+                                                 const RowCtx& rc)
+{
+	switch (rc.nf) {
+	case 0: return row_loop<NREG, 0>(a, w, lane, rc);
+	case 1: return row_loop<NREG, 1>(a, w, lane, rc);
+	case 2: return row_loop<NREG, 2>(a, w, lane, rc);
+	case 3: return row_loop<NREG, 3>(a, w, lane, rc);
+	case 4: return row_loop<NREG, 4>(a, w, lane, rc);
+	case 5: return row_loop<NREG, 5>(a, w, lane, rc);
+	case 6: return row_loop<NREG, 6>(a, w, lane, rc);
+	case 7: return row_loop<NREG, 7>(a, w, lane, rc);
+	case 8: return row_loop<NREG, 8>(a, w, lane, rc);
+	default: return row_loop<NREG, 9>(a, w, lane, rc);
+	}
+}
+
+template <int NREG>
+__global__ void __launch_bounds__(kSieveThreads, kSieveMinBlocks) k_sieve(const SieveArgs a)
 {
 	extern __shared__ uint4 s_dyn[];
-	__shared__ unsigned long long s_pairs;
+	__shared__ bool s_last;
+	__shared__ unsigned long long s_red[kSieveWarps];
 	const uint32_t lane = threadIdx.x & 31;
 	const uint32_t wib = threadIdx.x >> 5;
-	uint4* s_desc = s_dyn + static_cast<size_t>(wib) * a.np;  // per-warp {rowbase, r, m, -}
-	// per-CTA first-killer counts by probe index, after all warps' descriptors
-	unsigned long long* s_hist =
-	    reinterpret_cast<unsigned long long*>(s_dyn + static_cast<size_t>(kSieveWarps) * a.np);
+	WarpSmem w;
+	w.desc = s_dyn + static_cast<size_t>(wib) * a.np;
+	uint2* q_all = reinterpret_cast<uint2*>(s_dyn + static_cast<size_t>(kSieveWarps) * a.np);
+	w.queue = q_all + wib * kQueue;
+	uint32_t* h_all = reinterpret_cast<uint32_t*>(q_all + kSieveWarps * kQueue);
+	w.hist = h_all + static_cast<size_t>(wib) * a.np;
+	for (uint32_t j = lane; j < a.np; j += 32) w.hist[j] = 0;
+	__syncwarp();
 
-	for (uint32_t j = threadIdx.x; j < a.np; j += blockDim.x) s_hist[j] = 0;
-	if (threadIdx.x == 0) s_pairs = 0;
-	__syncthreads();
-
-	const unsigned long long W = a.prefix[a.n_slots];
+	const uint32_t n_chunks = plan_chunks(a.n_slots);
+	const unsigned long long W = a.chunk_off[n_chunks];
 	const unsigned long long nwarps = static_cast<unsigned long long>(gridDim.x) * kSieveWarps;
 	const unsigned long long gw = static_cast<unsigned long long>(blockIdx.x) * kSieveWarps + wib;
 	unsigned long long ws = W * gw / nwarps;  // W < 2^40, nwarps < 2^20
 	const unsigned long long we = W * (gw + 1) / nwarps;
 
-	// 32-ary warp search: largest slot s with prefix[s] <= ws
+	// 32-ary warp search: largest slot s with prefix(s) <= ws
 	uint32_t lo = 0, hi = a.n_slots;
 	if (ws < we) {
 		while (hi - lo > 1) {
 			const uint32_t step = (hi - lo + 31) / 32;
 			const uint32_t idx = lo + step * lane;
-			const bool le = idx < hi && a.prefix[idx] <= ws;
+			const bool le = idx < hi && slot_prefix(a, idx) <= ws;
 			const uint32_t L = 31 - __clz(__ballot_sync(kFull, le));
 			lo += step * L;
 			hi = min(hi, lo + step);
 		}
 	}
 
-	unsigned long long pairs = 0;
 	uint32_t slot = lo;
 	while (ws < we) {
-		const unsigned long long rs = a.prefix[slot], re = a.prefix[slot + 1];
+		const unsigned long long rs = slot_prefix(a, slot), re = slot_prefix(a, slot + 1);
 		if (re <= ws) {
 			++slot;
 			continue;
 		}
-		// this warp's share of the row's units; the first kRowCost are the
+		// this warp's share of the row's units; the first row_cost are the
 		// setup charge, the rest map 1:1 to windows
 		const unsigned long long u0 = ws - rs, u1 = min(we, re) - rs;
 		ws = min(we, re);
 		const uint32_t cur = slot++;
-		if (u1 <= kRowCost) continue;
-		const uint32_t w0 = static_cast<uint32_t>(u0 > kRowCost ? u0 - kRowCost : 0);
-		const uint32_t w1 = static_cast<uint32_t>(u1 - kRowCost);
+		const uint32_t rcost = a.row_cost;
+		if (u1 <= rcost) continue;
 		const RowBounds rb = slot_row(a, cur);
-		const uint32_t p = static_cast<uint32_t>(rb.p);
-		const uint32_t qlo = static_cast<uint32_t>(rb.qlo);
+		RowCtx rc;
+		rc.p = static_cast<uint32_t>(rb.p);
+		rc.qlo = static_cast<uint32_t>(rb.qlo);
 		const uint32_t qhi = static_cast<uint32_t>(rb.qhi);
+		rc.w0 = static_cast<uint32_t>(u0 > rcost ? u0 - rcost : 0);
+		rc.w1 = static_cast<uint32_t>(u1 - rcost);
+		rc.wlast = (qhi - rc.qlo) / 32;
+		rc.tail = (2u << (qhi - (rc.qlo + 32 * rc.wlast))) - 1;  // span 31 -> all ones
 
-		// ---- row setup: distinct prime factors of p (trial division) ----
-		uint32_t fac[kMaxFactors];
-		uint32_t nf = 0;
+		// ---- distinct prime factors of p (trial division, warp-parallel) ----
+		// f = 2 becomes a constant mask (the q step per lane is even); odd
+		// factors above qhi cannot divide any q of the row and are dropped.
+		rc.nf = 0;
+		bool even = false;
 		{
-			uint32_t cof = p;
+			uint32_t cof = rc.p;
 			for (uint32_t base = 0; base < a.n_fprimes; base += 32) {
 				const uint32_t i = base + lane;
 				uint2 fp = make_uint2(0xffffffffu, 0);
 				if (i < a.n_fprimes) fp = __ldg(a.fprimes + i);
-				const bool in_range = i < a.n_fprimes && static_cast<uint64_t>(fp.x) * fp.x <= p;
-				const bool divides = in_range && mod_full(p, fp.x, fp.y) == 0;
+				const bool in_range = i < a.n_fprimes && static_cast<uint64_t>(fp.x) * fp.x <= rc.p;
+				const bool divides = in_range && mod_full(rc.p, fp.x, fp.y) == 0;
 				uint32_t hits = __ballot_sync(kFull, divides);
 				while (hits) {
 					const uint32_t src = __ffs(hits) - 1;
 					hits &= hits - 1;
 					const uint32_t f = __shfl_sync(kFull, fp.x, src);
 					const uint32_t fm = __shfl_sync(kFull, fp.y, src);
-					if (nf < kMaxFactors) fac[nf] = f;
-					++nf;
-					// divide f out of the cofactor
-					for (;;) {
+					if (f == 2) even = true;
+					else if (f <= qhi && rc.nf < kMaxFactors) rc.fac[rc.nf++] = f;
+					for (;;) {  // divide f out of the cofactor
 						const uint32_t qt = __umulhi(cof, fm);
 						uint32_t rem = cof - qt * f, qq = qt;
 						if (rem >= f) { rem -= f; ++qq; }
@@ -204,141 +438,55 @@ __global__ void __launch_bounds__(kSieveThreads) k_sieve(const SieveArgs a)
 				}
 				if (!__any_sync(kFull, in_range)) break;
 			}
-			if (cof > 1 && nf < kMaxFactors) fac[nf++] = cof;  // the prime factor above sqrt(p)
+			// the prime factor above sqrt(p), if any
+			if (cof > 1 && cof <= qhi && rc.nf < kMaxFactors) rc.fac[rc.nf++] = cof;
 		}
-		// per-factor state: offset of the first multiple in the lane's window,
-		// per-step decrement, period pattern
-		uint32_t fo[kMaxFactors], fd[kMaxFactors], fpat[kMaxFactors], ff[kMaxFactors];
-		const uint32_t q0_first = qlo + 32 * (w0 + lane);
-#pragma unroll
-		for (int k = 0; k < kMaxFactors; ++k) {
-			if (k < nf) {
-				const uint32_t f = fac[k];
-				const uint32_t b = q0_first % f;
-				ff[k] = f;
-				fo[k] = b ? f - b : 0;
-				fd[k] = kStepQ % f;
-				fpat[k] = period_mask(f);
-			}
-		}
+		// q0 parity is fixed per lane (q advances by 32 per window): even p
+		// excludes the even q of every window
+		rc.even = even ? (((rc.qlo + 32 * (rc.w0 + lane)) & 1) ? 0xAAAAAAAAu : 0x55555555u) : 0u;
 
-		// ---- per-prime row bases: registers for the leading probes, smem for the rest
-		uint32_t rw0[NREG > 0 ? NREG : 1], rw1[NREG > 0 ? NREG : 1], rb_[NREG > 0 ? NREG : 1];
-		uint32_t cnt[NREG > 0 ? NREG : 1];
-#pragma unroll
-		for (int j = 0; j < NREG; ++j) {
-			const uint32_t r = a.reg_r[j], m = a.reg_m[j];
-			const uint32_t row = a.reg_base[j] + mod_full(p, r, m) * 2;  // S = 2 for r <= 31
-			rw0[j] = __ldg(a.ext + row);
-			rw1[j] = __ldg(a.ext + row + 1);
-			rb_[j] = mod_full(q0_first, r, m);
-			cnt[j] = 0;
-		}
+		// ---- deep probe descriptors for this row (rank order) ----
 		for (uint32_t j = NREG + lane; j < a.np; j += 32) {
 			const uint4 d = __ldg(a.probes + j);
-			s_desc[j] = make_uint4(d.z + mod_full(p, d.x, d.y) * d.w, d.x, d.y, 0);
+			w.desc[j] = make_uint4(d.z + mod_full(rc.p, d.x, d.y) * d.w, d.x, d.y, 0);
 		}
 		__syncwarp();
 
-		uint32_t deep_max = 0;  // 1 + largest deep probe index with a kill (0: none)
-		uint32_t row_pairs = 0;
-		const uint32_t n_iter = (w1 - w0 + 31) / 32;
-		for (uint32_t it = 0; it < n_iter; ++it) {
-			const uint32_t w = w0 + lane + 32 * it;
-			const uint32_t q0 = qlo + 32 * w;
-			uint32_t alive = 0;
-			if (w < w1) {
-				const uint32_t span = qhi - q0;  // q0 <= qhi for w < w1
-				alive = span >= 31 ? kFull : ((2u << span) - 1);
-				if (p == 1 && q0 == 1) alive &= ~1u;  // q == p (engine.hpp:258)
-			}
-			uint32_t nonc = 0;
-#pragma unroll
-			for (int k = 0; k < kMaxFactors; ++k) {
-				if (k < nf) {
-					nonc |= shl_clamp(fpat[k], fo[k]);
-					const uint32_t t = fo[k] - fd[k];
-					fo[k] = min(t, t + ff[k]);
-				}
-			}
-			alive &= ~nonc;
-			row_pairs += __popc(alive);
-#pragma unroll
-			for (int j = 0; j < NREG; ++j) {
-				const uint32_t M = __funnelshift_r(rw0[j], rw1[j], rb_[j]);
-				const uint32_t k = alive & M;
-				cnt[j] += __popc(k);
-				alive ^= k;
-				const uint32_t t = rb_[j] + a.reg_delta[j];
-				rb_[j] = min(t, t - a.reg_r[j]);
-			}
-			if (alive) {
-				for (uint32_t j = NREG; j < a.np; ++j) {
-					const uint4 d = s_desc[j];
-					const uint32_t b = mod_full(q0, d.y, d.z);
-					const uint32_t* wp = a.ext + d.x + (b >> 5);
-					const uint32_t M = __funnelshift_r(__ldg(wp), __ldg(wp + 1), b);
-					const uint32_t k = alive & M;
-					if (k) {
-						atomicAdd(&s_hist[j], static_cast<unsigned long long>(__popc(k)));
-						deep_max = max(deep_max, j + 1);
-						alive ^= k;
-						if (!alive) break;
-					}
-				}
-			}
-			// survivors: warp-aggregated reservation, then (p<<32)|q records
-			if (__any_sync(kFull, alive)) {
-				const uint32_t n = __popc(alive);
-				uint32_t x = n;
-#pragma unroll
-				for (int d = 1; d < 32; d <<= 1) {
-					const uint32_t y = __shfl_up_sync(kFull, x, d);
-					if (lane >= d) x += y;
-				}
-				const uint32_t total = __shfl_sync(kFull, x, 31);
-				unsigned long long base = 0;
-				if (lane == 31) base = atomicAdd(&a.counters[1], static_cast<unsigned long long>(total));
-				base = __shfl_sync(kFull, base, 31) + (x - n);
-				while (alive) {
-					const uint32_t bit = __ffs(alive) - 1;
-					alive &= alive - 1;
-					if (base < a.surv_cap)
-						a.surv[base] = (static_cast<unsigned long long>(p) << 32) | (q0 + bit);
-					++base;
-				}
-			}
-		}
-
-		// ---- row flush: histogram (register probes), block r_max
-		uint32_t kmax = 0;
-		bool any_kill = false;
-#pragma unroll
-		for (int j = 0; j < NREG; ++j) {
-			const uint32_t s = warp_sum(cnt[j]);
-			if (s) {
-				if (lane == 0) atomicAdd(&s_hist[j], static_cast<unsigned long long>(s));
-				kmax = j;
-				any_kill = true;
-			}
-		}
-		const uint32_t dmax = __reduce_max_sync(kFull, deep_max);
-		if (dmax) {
-			kmax = dmax - 1;
-			any_kill = true;
-		}
-		if (lane == 0 && any_kill) {
-			const uint32_t killer = kmax < NREG ? a.reg_r[kmax < NREG ? kmax : 0] : s_desc[kmax].y;
+		const uint32_t kk = dispatch_row<NREG>(a, w, lane, rc);  // 1 + deepest killer
+		if (lane == 0 && kk) {
+			const uint32_t j = kk - 1;
+			const uint32_t killer = j < NREG ? a.reg_r[j < NREG ? j : 0] : w.desc[j].y;
 			atomicMax(&a.block_rmax[rb.p / 100 - a.blk_lo], killer);
 		}
-		pairs += warp_sum(row_pairs);
 		__syncwarp();
 	}
-	if (lane == 0 && pairs) atomicAdd(&s_pairs, pairs);
+
+	// ---- CTA flush: per-warp counters -> global histogram ----
 	__syncthreads();
-	for (uint32_t j = threadIdx.x; j < a.np; j += blockDim.x)
-		if (s_hist[j]) atomicAdd(&a.hist[__ldg(a.probe_rank + j)], s_hist[j]);
-	if (threadIdx.x == 0 && s_pairs) atomicAdd(&a.counters[0], s_pairs);
+	for (uint32_t j = threadIdx.x; j < a.np; j += blockDim.x) {
+		unsigned long long s = 0;
+		for (int v = 0; v < kSieveWarps; ++v) s += h_all[static_cast<size_t>(v) * a.np + j];
+		if (s) atomicAdd(&a.hist[__ldg(a.probe_rank + j)], s);
+	}
+	// the last CTA: pairs_tested = sum(hist) + survivors
+	__threadfence();
+	__syncthreads();
+	if (threadIdx.x == 0) s_last = atomicAdd(&a.tickets[1], 1u) == gridDim.x - 1;
+	__syncthreads();
+	if (!s_last) return;
+	__threadfence();
+	unsigned long long s = 0;
+	for (uint32_t k = threadIdx.x; k < a.nprimes; k += blockDim.x)
+		s += *reinterpret_cast<volatile unsigned long long*>(a.hist + k);
+	for (int d = 16; d; d >>= 1) s += __shfl_xor_sync(kFull, s, d);
+	if (lane == 0) s_red[wib] = s;
+	__syncthreads();
+	if (threadIdx.x == 0) {
+		unsigned long long t = 0;
+		for (int v = 0; v < kSieveWarps; ++v) t += s_red[v];
+		a.counters[0] = t + *reinterpret_cast<volatile unsigned long long*>(a.counters + 1);
+		a.tickets[1] = 0;
+	}
 }
 
 // block r_max init: 1 for blocks owned by this shard, 0 otherwise
@@ -397,7 +545,8 @@ void* sieve_kernel_ptr(int nreg)
 
 size_t sieve_smem_bytes(uint32_t np)
 {
-	return sizeof(uint4) * static_cast<size_t>(np) * kSieveWarps + sizeof(unsigned long long) * np;
+	return (sizeof(uint4) + sizeof(uint32_t)) * static_cast<size_t>(np) * kSieveWarps +
+	       sizeof(uint2) * kQueue * kSieveWarps;
 }
 
 int sieve_grid(int device, int nreg, size_t smem)
@@ -412,9 +561,9 @@ int sieve_grid(int device, int nreg, size_t smem)
 	return sms * per_sm;
 }
 
-cudaError_t launch_plan(const SieveArgs& a, unsigned long long* d_prefix, cudaStream_t s)
+cudaError_t launch_plan(const SieveArgs& a, cudaStream_t s)
 {
-	k_plan<<<1, 1024, 0, s>>>(a, d_prefix);
+	k_plan<<<plan_chunks(a.n_slots), kPlanChunk, 0, s>>>(a);
 	return cudaGetLastError();
 }
 
