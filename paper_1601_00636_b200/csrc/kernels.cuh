@@ -43,6 +43,7 @@ cudaError_t launch_check_padding(const PrimeJob* d_jobs, uint32_t njobs, const u
                                  uint32_t* d_bad, cudaStream_t s);
 
 constexpr uint32_t kCubeThreads = 256;
+constexpr int kCubePairs = 4;  // (a,b) pairs per thread in k_cube
 constexpr uint32_t kPermThreads = 256;
 constexpr uint32_t kRow1Threads = 128;
 constexpr uint32_t kDeriveThreads = 256;
@@ -51,10 +52,10 @@ constexpr uint32_t kDeriveThreads = 256;
 
 constexpr int kSieveThreads = 256;
 #ifndef CGPU_SIEVE_MIN_BLOCKS
-#define CGPU_SIEVE_MIN_BLOCKS 3
+#define CGPU_SIEVE_MIN_BLOCKS 2
 #endif
 constexpr int kSieveMinBlocks = CGPU_SIEVE_MIN_BLOCKS;  // CTAs per SM the register budget targets
-constexpr uint32_t kDefaultRowCost = 400;                 // window-equivalents per row setup
+constexpr uint32_t kDefaultRowCost = 600;                 // window-equivalents per row setup
 constexpr int kSieveWarps = kSieveThreads / 32;
 constexpr int kMaxReg = 8;      // leading probes held in registers (r <= 31)
 constexpr int kMaxFactors = 9;  // distinct prime factors of p < 2^32

@@ -63,35 +63,78 @@ __device__ __forceinline__ void store_word_bytes(uint8_t* table, uint32_t tbytes
 	}
 }
 
-// Exhaustive cube (sievetable.hpp:102-115 semantics, every t evaluated): one
-// thread per (a,b), all t in [0, r). s = t^2 mod r is hoisted into shared
-// memory and read as a broadcast.
+// Exhaustive cube (sievetable.hpp:102-115 semantics, every t evaluated): the
+// bit of (a,b) is 1 iff Q_ab(t) != 0 mod r for all t in Z_r. Each thread owns
+// kCubePairs pairs (a,b) (strided by the CTA width so every ballot covers 32
+// consecutive bits of the reference's global index) and evaluates
+//     Q = s^5 + c4 s^4 + c3 s^3 + c2 s^2 + c1 s + c0   (s = t^2, modpoly.hpp:3-11)
+// at every t. The powers s^k mod r depend only on t, so they are tabulated
+// once per CTA in shared memory and read as broadcasts; the evaluation is then
+// four IMADs into an accumulator < 4r^2 + r < 2^24 and ONE Barrett reduction,
+// compared against -c0 mod r (the lazy remainder lies in [0, 2r)). Same value
+// as the reference's Horner (modpoly.hpp:116-125), half the multiplies.
 __global__ void __launch_bounds__(kCubeThreads) k_cube(const PrimeJob* __restrict__ jobs,
                                                        uint8_t* __restrict__ packed)
 {
-	extern __shared__ uint16_t s_sq[];
+	extern __shared__ uint4 s_pw[];  // [r] {s, s^2, s^3, s^4} then [r] s^5
 	const PrimeJob job = jobs[blockIdx.y];
 	const uint32_t r = job.r, m = job.m;
-	for (uint32_t t = threadIdx.x; t < r; t += blockDim.x) s_sq[t] = mod_full(t * t, r, m);
-	__syncthreads();
 	const uint32_t rr = r * r;
+	const uint32_t per_cta = kCubeThreads * kCubePairs;
+	if (blockIdx.x * per_cta >= rr) return;
+	uint32_t* s_p5 = reinterpret_cast<uint32_t*>(s_pw + r);
+	for (uint32_t t = threadIdx.x; t < r; t += blockDim.x) {
+		const uint32_t s1 = mod_full(t * t, r, m);
+		const uint32_t s2 = mod_full(s1 * s1, r, m);
+		const uint32_t s3 = mod_full(s2 * s1, r, m);
+		const uint32_t s4 = mod_full(s3 * s1, r, m);
+		s_pw[t] = make_uint4(s1, s2, s3, s4);
+		s_p5[t] = mod_full(s4 * s1, r, m);
+	}
+	__syncthreads();
 	const uint32_t tbytes = (rr + 7) >> 3;
 	const uint32_t lane = threadIdx.x & 31;
-	for (uint32_t base = blockIdx.x * kCubeThreads; base < rr; base += gridDim.x * kCubeThreads) {
-		const uint32_t i = base + threadIdx.x;
-		const bool valid = i < rr;
-		uint32_t a = __umulhi(i, m), b = i - a * r;
-		if (b >= r) { b -= r; ++a; }
-		uint32_t c[5];
-		mod_coeffs(valid ? a : 0, valid ? b : 0, r, m, c);
-		bool hit = false;
-#pragma unroll 4
-		for (uint32_t t = 0; t < r; ++t) {
-			const uint32_t v = horner_lazy(c, s_sq[t], r, m);
-			hit |= (v == 0) | (v == r);
+	uint32_t nr;  // x - q r as one IMAD x + q * (2^32 - r); opaque so it is not re-negated
+	asm("mov.b32 %0, %1;" : "=r"(nr) : "r"(0u - r));
+	for (uint32_t base = blockIdx.x * per_cta; base < rr; base += gridDim.x * per_cta) {
+		uint32_t c1[kCubePairs], c2[kCubePairs], c3[kCubePairs], c4[kCubePairs], nz[kCubePairs];
+		uint32_t mn[kCubePairs];  // min over t of (Q mod r) - (-c0): 0 iff some t is a root
+		bool valid[kCubePairs];
+#pragma unroll
+		for (int k = 0; k < kCubePairs; ++k) {
+			const uint32_t i = base + k * kCubeThreads + threadIdx.x;
+			valid[k] = i < rr;
+			uint32_t a = __umulhi(i, m), b = i - a * r;
+			if (b >= r) { b -= r; ++a; }
+			uint32_t c[5];
+			mod_coeffs(valid[k] ? a : 0, valid[k] ? b : 0, r, m, c);
+			c4[k] = c[0];
+			c3[k] = c[1];
+			c2[k] = c[2];
+			c1[k] = c[3];
+			nz[k] = 0u - (c[4] ? r - c[4] : 0);  // Q == 0 <=> s^5 + ... + c1 s == -c0 (mod r)
+			mn[k] = 0xffffffffu;
 		}
-		const uint32_t word = __ballot_sync(kFull, valid && !hit);
-		store_word_bytes(packed + job.byte_off, tbytes, base + (threadIdx.x & ~31u), word, lane);
+#pragma unroll 2
+		for (uint32_t t = 0; t < r; ++t) {
+			const uint4 p = s_pw[t];
+			const uint32_t p5 = s_p5[t];
+#pragma unroll
+			for (int k = 0; k < kCubePairs; ++k) {
+				uint32_t acc = c4[k] * p.w + p5;
+				acc = c3[k] * p.z + acc;
+				acc = c2[k] * p.y + acc;
+				acc = c1[k] * p.x + acc;
+				const uint32_t x = acc + __umulhi(acc, m) * nr;  // [0, 2r)
+				mn[k] = min(min(x, x - r) + nz[k], mn[k]);       // two VIADDMNMX
+			}
+		}
+#pragma unroll
+		for (int k = 0; k < kCubePairs; ++k) {
+			const uint32_t word = __ballot_sync(kFull, valid[k] && mn[k] != 0);
+			const uint32_t i0 = base + k * kCubeThreads + (threadIdx.x & ~31u);
+			store_word_bytes(packed + job.byte_off, tbytes, i0, word, lane);
+		}
 	}
 }
 
@@ -216,8 +259,12 @@ cudaError_t launch_cube(const PrimeJob* d_jobs, uint32_t njobs, uint32_t max_rr,
                         cudaStream_t s)
 {
 	if (!njobs) return cudaSuccess;
-	const dim3 grid(grid_x(max_rr, kCubeThreads, 4096), njobs);
-	const size_t smem = sizeof(uint16_t) * kModulusLimit;
+	const dim3 grid(grid_x(max_rr, kCubeThreads * kCubePairs, 8192), njobs);
+	uint32_t max_r = 1;
+	while (max_r * max_r < max_rr) ++max_r;
+	const size_t smem = (sizeof(uint4) + sizeof(uint32_t)) * max_r;  // 32 KB at r = 1621
+	if (smem > 48 * 1024)
+		cudaFuncSetAttribute(k_cube, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
 	k_cube<<<grid, kCubeThreads, smem, s>>>(d_jobs, d_packed);
 	return cudaGetLastError();
 }
