@@ -48,7 +48,8 @@ typedef enum {
 	CGPU_ERR_FORMAT = -4,        /* FormatError (sievetable.hpp:37-39) */
 	CGPU_ERR_RANGE = -5,         /* std::out_of_range */
 	CGPU_ERR_CAPACITY = -6,      /* caller's output buffer too small; sizes still reported */
-	CGPU_ERR_NO_DEVICE = -7      /* no CUDA device: this library has no CPU fallback */
+	CGPU_ERR_NO_DEVICE = -7,     /* no CUDA device: this library has no CPU fallback */
+	CGPU_ERR_IO = -8             /* file I/O failure (read_bytes / write_bytes, sievetable.hpp:313-332) */
 } cgpu_status;
 
 /* Row-bound modes of the sieve. REGION = the reference scan() region
@@ -106,6 +107,26 @@ int cgpu_tables_info(cgpu_ctx* ctx, uint32_t* n, uint8_t* killable);
 /* Stateless convenience: build on a temporary context of `device`. */
 int cgpu_build_tables(int device, const uint32_t* primes, uint32_t n, int algorithm,
                       uint8_t* out_bytes, uint32_t* out_offsets, uint64_t* out_evals);
+
+/* ---- on-disk formats (host; sievetable.hpp:229-346, proj/README.md) ---- */
+
+/* The CUPQ v1 index of a prime list (serialize_index, sievetable.hpp:231-252):
+ * 9-byte header ("CUPQ", 0x01, u32 LE count) + per prime {u16 LE prime, u32 LE
+ * byte offset}. out may be NULL (size query into *out_len). */
+int cgpu_index_serialize(const uint32_t* primes, uint32_t n, uint8_t* out, uint64_t cap,
+                         uint64_t* out_len);
+
+/* Validates an index exactly like load_sieve (sievetable.hpp:254-292; every
+ * violation is CGPU_ERR_FORMAT) and returns its primes (up to cap; primes may
+ * be NULL), the count and the tables-stream length the index implies. */
+int cgpu_index_parse(const uint8_t* index, uint64_t len, uint32_t* primes, uint32_t cap,
+                     uint32_t* n_out, uint64_t* tables_bytes);
+
+/* load_sieve_files / save_sieve_files (sievetable.hpp:334-346) for the device:
+ * reads a tables .bin + CUPQ index and makes the set resident; writes the
+ * resident set back byte-identically. */
+int cgpu_tables_load_files(cgpu_ctx* ctx, const char* tables_path, const char* index_path);
+int cgpu_tables_save_files(cgpu_ctx* ctx, const char* tables_path, const char* index_path);
 
 /* ---- sieve ------------------------------------------------------------- */
 

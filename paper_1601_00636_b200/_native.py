@@ -14,8 +14,8 @@ LIB_PATH = os.environ.get("CUBOID_GPU_LIB", os.path.join(HERE, "libcuboid_gpu.so
 # status codes (cuboid_gpu.h)
 OK = 0
 P_BELOW_152, P_ABOVE_LIMIT, Q_BELOW_LOW, Q_ABOVE_HIGH, NOT_LOADED = 2, 3, 4, 5, 6
-ERR_CUDA, ERR_INVALID, ERR_OVERFLOW, ERR_FORMAT, ERR_RANGE, ERR_CAPACITY, ERR_NO_DEVICE = (
-    -1, -2, -3, -4, -5, -6, -7)
+ERR_CUDA, ERR_INVALID, ERR_OVERFLOW, ERR_FORMAT, ERR_RANGE, ERR_CAPACITY, ERR_NO_DEVICE, ERR_IO = (
+    -1, -2, -3, -4, -5, -6, -7, -8)
 REGION, TRIANGLE = 0, 1
 BUILD_PRODUCTION, BUILD_EXHAUSTIVE = 0, 1
 
@@ -38,6 +38,10 @@ SIGNATURES = {
     "cgpu_tables_info": (C.c_int, [C.c_void_p, _u32p, C.c_void_p]),
     "cgpu_build_tables": (C.c_int, [C.c_int, C.c_void_p, C.c_uint32, C.c_int, C.c_void_p,
                                     C.c_void_p, _u64p]),
+    "cgpu_index_serialize": (C.c_int, [C.c_void_p, C.c_uint32, C.c_void_p, C.c_uint64, _u64p]),
+    "cgpu_index_parse": (C.c_int, [C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint32, _u32p, _u64p]),
+    "cgpu_tables_load_files": (C.c_int, [C.c_void_p, C.c_char_p, C.c_char_p]),
+    "cgpu_tables_save_files": (C.c_int, [C.c_void_p, C.c_char_p, C.c_char_p]),
     "cgpu_sieve_launch": (C.c_int, [C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint64, C.c_int,
                                     C.c_uint32, C.c_uint32, C.c_uint64]),
     "cgpu_sieve_results": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64,

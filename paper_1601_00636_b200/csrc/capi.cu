@@ -6,6 +6,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <fstream>
 #include <string>
 #include <vector>
 
@@ -110,6 +111,10 @@ void q_bounds(uint64_t p, uint64_t* lo, uint64_t* hi)  // region.hpp:49-63
 		*lo = q_lower_cubic(p);
 	}
 }
+
+constexpr uint64_t kIndexHeaderSize = 9;  // sievetable.hpp:148-151
+constexpr uint64_t kIndexRecordSize = 6;
+constexpr uint8_t kIndexVersion = 1;
 
 constexpr uint32_t kMaxSlots = 1u << 20;  // row slots per plan/sieve launch (multiple of 100 below)
 constexpr uint32_t kBlocksPerLaunch = kMaxSlots / 100;
@@ -472,6 +477,122 @@ int cgpu_tables_download(cgpu_ctx* c, uint8_t* out, uint64_t cap)
 		CK(cudaMemcpyAsync(out, c->packed.p, c->total_bytes, cudaMemcpyDeviceToHost, c->stream));
 		CK(cudaStreamSynchronize(c->stream));
 	}
+	return CGPU_OK;
+}
+
+// ---- on-disk formats (sievetable.hpp:229-346; proj/README.md "File formats") ----
+
+int cgpu_index_serialize(const uint32_t* primes, uint32_t n, uint8_t* out, uint64_t cap, uint64_t* out_len)
+{
+	uint64_t total = 0;
+	if (int rc = layout(primes, n, nullptr, &total)) return rc;
+	const uint64_t len = kIndexHeaderSize + kIndexRecordSize * static_cast<uint64_t>(n);
+	if (out_len) *out_len = len;
+	if (!out) return CGPU_OK;
+	if (cap < len) return set_err(CGPU_ERR_CAPACITY, "index buffer too small");
+	std::memcpy(out, "CUPQ", 4);
+	out[4] = kIndexVersion;
+	for (int b = 0; b < 4; ++b) out[5 + b] = static_cast<uint8_t>(n >> (8 * b));
+	uint64_t off = 0;
+	for (uint32_t k = 0; k < n; ++k) {
+		uint8_t* rec = out + kIndexHeaderSize + kIndexRecordSize * k;
+		rec[0] = static_cast<uint8_t>(primes[k]);
+		rec[1] = static_cast<uint8_t>(primes[k] >> 8);
+		for (int b = 0; b < 4; ++b) rec[2 + b] = static_cast<uint8_t>(off >> (8 * b));
+		off += table_bytes(primes[k]);
+	}
+	return CGPU_OK;
+}
+
+int cgpu_index_parse(const uint8_t* index, uint64_t len, uint32_t* primes, uint32_t cap, uint32_t* n_out,
+                     uint64_t* tables_bytes)
+{
+	if (!index && len) return set_err(CGPU_ERR_INVALID, "null index");
+	if (len < kIndexHeaderSize) return set_err(CGPU_ERR_FORMAT, "load_sieve: index truncated");
+	if (std::memcmp(index, "CUPQ", 4) != 0) return set_err(CGPU_ERR_FORMAT, "load_sieve: bad index magic");
+	if (index[4] != kIndexVersion)
+		return set_err(CGPU_ERR_FORMAT, "load_sieve: unsupported index version");
+	uint32_t n = 0;
+	for (int b = 0; b < 4; ++b) n |= static_cast<uint32_t>(index[5 + b]) << (8 * b);
+	if (len != kIndexHeaderSize + kIndexRecordSize * static_cast<uint64_t>(n))
+		return set_err(CGPU_ERR_FORMAT, "load_sieve: index length does not match record count");
+	if (n_out) *n_out = n;
+	uint64_t expect = 0;
+	uint32_t prev = 0;
+	for (uint32_t k = 0; k < n; ++k) {
+		const uint8_t* rec = index + kIndexHeaderSize + kIndexRecordSize * k;
+		const uint32_t prime = static_cast<uint32_t>(rec[0]) | static_cast<uint32_t>(rec[1]) << 8;
+		uint32_t off = 0;
+		for (int b = 0; b < 4; ++b) off |= static_cast<uint32_t>(rec[2 + b]) << (8 * b);
+		if (!is_prime_u32(prime) || prime >= kModulusLimit)
+			return set_err(CGPU_ERR_FORMAT, "load_sieve: index entry is not an admissible prime");
+		if (prime <= prev) return set_err(CGPU_ERR_FORMAT, "load_sieve: primes not strictly increasing");
+		if (off != expect) return set_err(CGPU_ERR_FORMAT, "load_sieve: offset mismatch");
+		prev = prime;
+		expect += table_bytes(prime);
+		if (expect > UINT32_MAX) return set_err(CGPU_ERR_FORMAT, "load_sieve: cumulative size exceeds 2^32");
+		if (primes && k < cap) primes[k] = prime;
+	}
+	if (tables_bytes) *tables_bytes = expect;
+	if (primes && cap < n) return set_err(CGPU_ERR_CAPACITY, "prime buffer too small");
+	return CGPU_OK;
+}
+
+namespace {
+
+bool read_file(const char* path, std::vector<uint8_t>& out)
+{
+	std::ifstream f(path, std::ios::binary);
+	if (!f) return false;
+	f.seekg(0, std::ios::end);
+	const std::streamoff len = f.tellg();
+	f.seekg(0);
+	out.resize(static_cast<size_t>(len));
+	f.read(reinterpret_cast<char*>(out.data()), len);
+	return static_cast<bool>(f) || len == 0;
+}
+
+bool write_file(const char* path, const uint8_t* data, size_t len)
+{
+	std::ofstream f(path, std::ios::binary | std::ios::trunc);
+	if (!f) return false;
+	f.write(reinterpret_cast<const char*>(data), static_cast<std::streamsize>(len));
+	return static_cast<bool>(f);
+}
+
+}  // namespace
+
+int cgpu_tables_load_files(cgpu_ctx* c, const char* tables_path, const char* index_path)
+{
+	if (!c || !tables_path || !index_path) return set_err(CGPU_ERR_INVALID, "null argument");
+	std::vector<uint8_t> tb, ix;
+	if (!read_file(index_path, ix)) return set_err(CGPU_ERR_IO, std::string("cannot open: ") + index_path);
+	if (!read_file(tables_path, tb)) return set_err(CGPU_ERR_IO, std::string("cannot open: ") + tables_path);
+	uint32_t n = 0;
+	uint64_t expect = 0;
+	if (int rc = cgpu_index_parse(ix.data(), ix.size(), nullptr, 0, &n, &expect)) return rc;
+	std::vector<uint32_t> primes(n);
+	if (int rc = cgpu_index_parse(ix.data(), ix.size(), primes.data(), n, &n, &expect)) return rc;
+	if (tb.size() != expect)
+		return set_err(CGPU_ERR_FORMAT, "load_sieve: tables stream length does not match index");
+	return cgpu_tables_load(c, primes.data(), n, tb.data(), tb.size());
+}
+
+int cgpu_tables_save_files(cgpu_ctx* c, const char* tables_path, const char* index_path)
+{
+	if (!c || !tables_path || !index_path) return set_err(CGPU_ERR_INVALID, "null argument");
+	if (!c->loaded) return set_err(CGPU_NOT_LOADED, "tables not loaded");
+	std::vector<uint8_t> tb(c->total_bytes);
+	if (int rc = cgpu_tables_download(c, tb.data(), tb.size())) return rc;
+	uint64_t len = 0;
+	const uint32_t n = static_cast<uint32_t>(c->primes.size());
+	if (int rc = cgpu_index_serialize(c->primes.data(), n, nullptr, 0, &len)) return rc;
+	std::vector<uint8_t> ix(len);
+	if (int rc = cgpu_index_serialize(c->primes.data(), n, ix.data(), len, &len)) return rc;
+	if (!write_file(tables_path, tb.data(), tb.size()))
+		return set_err(CGPU_ERR_IO, std::string("write failed: ") + tables_path);
+	if (!write_file(index_path, ix.data(), ix.size()))
+		return set_err(CGPU_ERR_IO, std::string("write failed: ") + index_path);
 	return CGPU_OK;
 }
 

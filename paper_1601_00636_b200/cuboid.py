@@ -29,7 +29,7 @@ from typing import Callable, Optional
 import numpy as np
 
 from . import _native as N
-from .device import Device, q_bounds as _q_bounds
+from .device import Device, parse_index, q_bounds as _q_bounds, serialize_index as _serialize_index
 from .primes import default_primes
 
 MODULUS_LIMIT = 9697                  # primes.hpp:12
@@ -173,6 +173,31 @@ class SieveSet:
         i = (p % r) * r + (q % r)
         return bool((self._tables[self._offsets[rank] + (i >> 3)] >> (i & 7)) & 1)
 
+    # -- on-disk formats (sievetable.hpp:229-346) ---------------------------
+    def serialize_index(self) -> bytes:
+        return serialize_index(self)
+
+    def save_files(self, tables_path: str, index_path: str) -> None:
+        """save_sieve_files: the device-resident bytes, written through the C ABI."""
+        self.resident().save_files(tables_path, index_path)
+
+    @classmethod
+    def load_files(cls, tables_path: str, index_path: str, dev: int = 0) -> "SieveSet":
+        """load_sieve_files straight onto the device (FormatError on a bad pair)."""
+        d = device(dev)
+        d._owner = None
+        try:
+            d.load_files(tables_path, index_path)
+        except N.CudaSieveError as e:
+            if e.code in (N.ERR_FORMAT, N.ERR_INVALID):
+                raise FormatError(str(e)) from e
+            if e.code == N.ERR_IO:
+                raise OSError(str(e)) from e
+            raise
+        s = cls(d.primes, d.download(), d.offsets, dev)
+        d._owner = id(s)
+        return s
+
     # -- device residency --------------------------------------------------
     def resident(self) -> Device:
         """The device context with this set loaded (re-uploads if another set
@@ -182,6 +207,40 @@ class SieveSet:
             d.load(self._primes, self._tables)
             d._owner = id(self)
         return d
+
+
+def serialize_index(set_: "SieveSet") -> bytes:
+    """serialize_index (sievetable.hpp:231-252)."""
+    return _serialize_index(set_.primes())
+
+
+def dump_table_text(set_: "SieveSet", r: int) -> str:
+    """Text rendering of one table, rows by p residue (sievetable.hpp:296-311)."""
+    rank = set_.rank_of(r)
+    if rank is None:
+        raise ValueError("dump_table_text: prime not in set")
+    t = set_.table_at(rank)
+    lines = [f"r={r}"]
+    for p in range(r):
+        lines.append(f"{p}: " + "".join("1" if t.bit(p, q) else "0" for q in range(r)))
+    return "\n".join(lines) + "\n"
+
+
+def serialize_tables(set_: "SieveSet") -> bytes:
+    """serialize_tables (sievetable.hpp:229)."""
+    return set_.tables()
+
+
+def load_sieve(tables: bytes, index: bytes, dev: int = 0) -> "SieveSet":
+    """load_sieve (sievetable.hpp:254-292): validates the index, then makes the
+    set resident. FormatError on any violation."""
+    try:
+        primes, total = parse_index(index)
+    except N.CudaSieveError as e:
+        raise FormatError(str(e)) from e
+    if len(tables) != total:
+        raise FormatError("load_sieve: tables stream length does not match index")
+    return SieveSet.from_parts(primes, tables, dev)
 
 
 @dataclass

@@ -84,6 +84,17 @@ class Device:
         self.primes = pr.copy()
         self.offsets, self.total_bytes = self.layout(pr)
 
+    def save_files(self, tables_path: str, index_path: str):
+        """save_sieve_files of the resident set (sievetable.hpp:334-339)."""
+        N.check(N.lib().cgpu_tables_save_files(self._ctx, tables_path.encode(), index_path.encode()))
+
+    def load_files(self, tables_path: str, index_path: str):
+        """load_sieve_files onto the device (sievetable.hpp:341-346)."""
+        N.check(N.lib().cgpu_tables_load_files(self._ctx, tables_path.encode(), index_path.encode()))
+        with open(index_path, "rb") as f:
+            self.primes = np.array(parse_index(f.read())[0], np.uint32)
+        self.offsets, self.total_bytes = self.layout(self.primes)
+
     def download(self) -> bytes:
         out = np.zeros(max(self.total_bytes, 1), np.uint8)
         N.check(N.lib().cgpu_tables_download(self._ctx, _ptr(out), self.total_bytes))
@@ -144,6 +155,28 @@ class Device:
         out = np.zeros(max(len(a), 1), np.int32)
         N.check(N.lib().cgpu_classify(self._ctx, _ptr(a), len(a), _ptr(out)))
         return out[: len(a)]
+
+
+def serialize_index(primes) -> bytes:
+    """CUPQ v1 index bytes (serialize_index, sievetable.hpp:231-252). Host-only."""
+    pr = np.ascontiguousarray(primes, dtype=np.uint32)
+    n = C.c_uint64()
+    N.check(N.lib().cgpu_index_serialize(_ptr(pr), len(pr), None, 0, C.byref(n)))
+    out = np.zeros(n.value, np.uint8)
+    N.check(N.lib().cgpu_index_serialize(_ptr(pr), len(pr), _ptr(out), n.value, C.byref(n)))
+    return out.tobytes()
+
+
+def parse_index(index: bytes):
+    """Validates like load_sieve (sievetable.hpp:254-292); returns (primes,
+    tables stream length). Raises CudaSieveError(ERR_FORMAT) on a bad index."""
+    buf = np.frombuffer(index, np.uint8) if len(index) else np.zeros(1, np.uint8)
+    n, total = C.c_uint32(), C.c_uint64()
+    N.check(N.lib().cgpu_index_parse(_ptr(buf), len(index), None, 0, C.byref(n), C.byref(total)))
+    pr = np.zeros(max(n.value, 1), np.uint32)
+    N.check(N.lib().cgpu_index_parse(_ptr(buf), len(index), _ptr(pr), n.value, C.byref(n),
+                                     C.byref(total)))
+    return [int(x) for x in pr[: n.value]], total.value
 
 
 def q_bounds(p: int):

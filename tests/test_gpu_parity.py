@@ -309,3 +309,54 @@ def test_sharded_sieve_single_rank(dev):
     assert (pairs, surv) == (o["pairs_tested"], o["survivors"])
     assert hist.tolist() == o["hist"].astype(np.int64).tolist()
     assert np.array_equal(sp, o["survivor_pairs"])
+
+
+def test_files_roundtrip_with_reference(tmp_path, sets):
+    """GPU-built tables written through the C ABI are the reference's files
+    (save_sieve_files / load_sieve_files, test_sievetable.cpp:240-262), and
+    reference-written files load onto the device and sieve identically."""
+    P = sets["default96"]
+    s = cuboid.SieveSet.build(P)
+    tp, ip = str(tmp_path / "tables.bin"), str(tmp_path / "primes.bin")
+    s.save_files(tp, ip)
+    tb, ix = open(tp, "rb").read(), open(ip, "rb").read()
+    assert tb == port.build_set(P)[0]
+    assert ix == s.serialize_index()
+    if refmod.available():
+        rs = refmod.RefSet.load(tb, ix)
+        assert rs.tables() == tb and rs.index_bytes() == ix
+    back = cuboid.SieveSet.load_files(tp, ip)
+    assert back.primes() == P and back.tables() == tb
+    st = cuboid.scan(back, (152, 3), 300)
+    assert st.survivors == 0 and st.pairs_tested == cuboid.scan(s, (152, 3), 300).pairs_tested
+    with pytest.raises(OSError):
+        cuboid.SieveSet.load_files(str(tmp_path / "missing.bin"), ip)
+    with pytest.raises(cuboid.FormatError):
+        cuboid.load_sieve(tb[:-1], ix)
+    empty = cuboid.load_sieve(b"", cuboid.serialize_index(cuboid.SieveSet([], b"", [], 0)))
+    assert empty.empty()
+
+
+def test_dump_table_text_matches_u11():
+    """test_sievetable.cpp:222-238: the text dump of r = 11 is the paper's U_11."""
+    s = cuboid.SieveSet.build([2, 11])
+    txt = cuboid.dump_table_text(s, 11).splitlines()
+    assert txt[0] == "r=11"
+    want = port.build_table(11)
+    for p in range(11):
+        row = txt[1 + p].split(": ")[1]
+        assert row == "".join(str((want[(p * 11 + q) >> 3] >> ((p * 11 + q) & 7)) & 1) for q in range(11))
+    assert cuboid.dump_table_text(s, 2) == "r=2\n0: 00\n1: 00\n"
+
+
+def test_historical_region_scan():
+    """p = 1..154000 over the full region with the 96 primes
+    11..541: no pair passes the sieve and the deepest first killer is 137 (the
+    29th prime of the set)."""
+    s = cuboid.SieveSet.build_default()
+    st = cuboid.scan(s, (1, 1), 154000, opt=cuboid.ScanOptions(small_p=True))
+    assert st.survivors == 0
+    assert max(st.kill_histogram) == 137
+    assert max(st.block_r_max.values()) == 137
+    assert len(st.block_r_max) == 1541
+    assert st.histogram_total() == st.pairs_tested
