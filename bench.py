@@ -220,12 +220,17 @@ def run_ours(args, wl, primes):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.same_device:  # plumbing test only: every rank on GPU 0, gloo collectives on the CPU
+        local = 0
+    torch.cuda.set_device(local)
+    gloo = args.backend == "gloo"
     if world > 1:
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    else:
-        torch.cuda.set_device(local)
+        if gloo:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     cuda = torch.device("cuda", local)
+    cdev = torch.device("cpu") if gloo else cuda  # where collectives run
     stream = torch.cuda.Stream(device=cuda)  # the context and all torch work share it
     torch.cuda.set_stream(stream)
     L = N.lib()
@@ -233,13 +238,17 @@ def run_ours(args, wl, primes):
     def allreduce_max(x: float) -> float:
         if world == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device=cuda)
+        t = torch.tensor([x], dtype=torch.float64, device=cdev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
     def barrier():
+        torch.cuda.synchronize()
         if world > 1:
-            dist.barrier(device_ids=[local])
+            if gloo:
+                dist.barrier()
+            else:
+                dist.barrier(device_ids=[local])
         torch.cuda.synchronize()
 
     dev = Device(local, stream=stream.cuda_stream)
@@ -283,6 +292,28 @@ def run_ours(args, wl, primes):
                      "note": "SURVEY 8(d) counts 27 INT32 ops/eval for Horner; the kernel needs 8"},
     }
 
+    # ---- the paper's historical scan, for the published figure ------
+    historical = None
+    if world == 1:
+        from paper_1601_00636_b200.primes import default_primes
+        DP = default_primes()
+        dev.build(DP, N.BUILD_PRODUCTION, download=False)
+        hms = []
+        for i in range(3):
+            r = dev.sieve(1, 154000, N.REGION, surv_cap=1 << 16)
+            hms.append(dev.timings_ms()["sieve"])
+        hk = max((DP[k] for k, c in enumerate(r.hist) if c), default=0)
+        t_h = min(hms) * 1e-3
+        prefilter = sum(59 * p for p in range(1, 154001))  # the paper's N = 699,626,543,000
+        historical = {
+            "config": "REGION scan p=1..154000, q_low(p)<=q<=59p, 96 primes 11..541 (PAPER.md:852-870)",
+            "pairs_tested": r.pairs_tested, "survivors": r.survivors, "max_killer": hk,
+            "kernel_ms": 1e3 * t_h, "pairs_per_s": r.pairs_tested / t_h,
+            "sec_per_prefilter_pair": t_h / prefilter, "paper_sec_per_pair": 3.54e-7,
+            "paper_wall": "4130 min on a Pentium 4 (1 thread)",
+            "pin_ok": r.survivors == 0 and hk == 137,
+        }
+
     # ---- resident set for the workload ------------------------------------------------
     tables, _ = dev.build(primes, N.BUILD_PRODUCTION)
     killable = dev.killable()
@@ -302,10 +333,19 @@ def run_ours(args, wl, primes):
             nblocks, C.c_void_p(surv.data_ptr()), GATHER_CAP))
 
     def exchange():
-        if world > 1:
+        if world > 1 and not gloo:
             dist.all_reduce(acc, op=dist.ReduceOp.SUM)
             dist.all_reduce(brm, op=dist.ReduceOp.MAX)
             dist.all_gather_into_tensor(gath, surv)
+        elif world > 1:  # gloo: stage through host memory
+            a, b, sv = acc.cpu(), brm.cpu(), surv.cpu()
+            gv = torch.zeros(GATHER_CAP * world, dtype=torch.int64)
+            dist.all_reduce(a, op=dist.ReduceOp.SUM)
+            dist.all_reduce(b, op=dist.ReduceOp.MAX)
+            dist.all_gather_into_tensor(gv, sv)
+            acc.copy_(a)
+            brm.copy_(b)
+            gath.copy_(gv)
 
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
@@ -414,6 +454,7 @@ def run_ours(args, wl, primes):
             "gpu_launches": launches,
             "roofline": roof,
             "table_build": table_build,
+            "historical_region_scan": historical,
             "clocks": clk.summary(),
         }
         if world == 1 and not args.no_cpu_baseline:
@@ -439,6 +480,9 @@ def main():
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="C5")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0, help="seconds of CPU sample")
+    ap.add_argument("--backend", choices=["nccl", "gloo"], default="nccl")
+    ap.add_argument("--same-device", action="store_true",
+                    help="plumbing test: all ranks on GPU 0 (use with --backend gloo)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     from paper_1601_00636_b200.primes import odd_primes
