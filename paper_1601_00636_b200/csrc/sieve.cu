@@ -25,6 +25,8 @@
 // the rare deep probes run at full SIMD width. Tables that never kill
 // (all-zero, e.g. r = 3, 5, 7) are not probed -- identical results.
 
+#include <cuda/std/type_traits>
+
 #include "../../include/cuboid_gpu.h"
 #include "common.cuh"
 #include "kernels.cuh"
@@ -251,9 +253,11 @@ template <int NREG, int NF>
 __device__ __forceinline__ uint32_t row_loop(const SieveArgs& a, const WarpSmem& w, uint32_t lane,
                                              const RowCtx& rc)
 {
-	uint32_t cnt[NREG > 0 ? NREG : 1];
+	// S[j] = sum over this lane's windows of popc(alive before register probe j);
+	// probe j's first-kill count is S[j] - S[j+1] (telescoping: one LOP3 per probe)
+	uint32_t S[NREG + 1];
 #pragma unroll
-	for (int j = 0; j < NREG; ++j) cnt[j] = 0;
+	for (int j = 0; j <= NREG; ++j) S[j] = 0;
 	uint32_t kmax = 0;
 	const uint32_t q0_first = rc.qlo + 32 * (rc.w0 + lane);
 	uint32_t fo[NF > 0 ? NF : 1], fd[NF > 0 ? NF : 1], fpat[NF > 0 ? NF : 1], ff[NF > 0 ? NF : 1];
@@ -277,11 +281,12 @@ __device__ __forceinline__ uint32_t row_loop(const SieveArgs& a, const WarpSmem&
 	}
 	const uint32_t lt = (1u << lane) - 1;
 	uint32_t qn = 0;  // queued windows
-	const uint32_t n_iter = (rc.w1 - rc.w0 + 31) / 32;
-	for (uint32_t it = 0; it < n_iter; ++it) {
+
+	// one window per lane; EDGE iterations also mask the row's partial last
+	// window and lanes past the warp's slice
+	auto step = [&](uint32_t it, auto edge) {
 		const uint32_t wi = rc.w0 + lane + 32 * it;
 		const uint32_t q0 = rc.qlo + 32 * wi;
-		uint32_t alive = wi < rc.w1 ? (wi < rc.wlast ? kFull : rc.tail) : 0u;
 		uint32_t nonc = rc.even;
 #pragma unroll
 		for (int k = 0; k < NF; ++k) {
@@ -289,13 +294,13 @@ __device__ __forceinline__ uint32_t row_loop(const SieveArgs& a, const WarpSmem&
 			const uint32_t t = fo[k] - fd[k];
 			fo[k] = min(t, t + ff[k]);
 		}
-		alive &= ~nonc;
+		uint32_t alive = ~nonc;
+		if constexpr (decltype(edge)::value) alive &= wi < rc.w1 ? (wi < rc.wlast ? kFull : rc.tail) : 0u;
+		S[0] += __popc(alive);
 #pragma unroll
 		for (int j = 0; j < NREG; ++j) {
-			const uint32_t M = __funnelshift_r(rw0[j], rw1[j], rb[j]);
-			const uint32_t k = alive & M;
-			cnt[j] += __popc(k);
-			alive ^= k;
+			alive &= ~__funnelshift_r(rw0[j], rw1[j], rb[j]);
+			S[j + 1] += __popc(alive);
 			const uint32_t t = rb[j] + a.reg_delta[j];
 			rb[j] = min(t, t - a.reg_r[j]);
 		}
@@ -310,7 +315,13 @@ __device__ __forceinline__ uint32_t row_loop(const SieveArgs& a, const WarpSmem&
 				__syncwarp();
 			}
 		}
-	}
+	};
+	const uint32_t n_iter = (rc.w1 - rc.w0 + 31) / 32;
+	const uint32_t E = min(rc.w1, rc.wlast);  // windows below E are whole and in the slice
+	const uint32_t n_full = E > rc.w0 ? min((E - rc.w0) / 32, n_iter) : 0;
+	uint32_t it = 0;
+	for (; it < n_full; ++it) step(it, cuda::std::false_type{});
+	for (; it < n_iter; ++it) step(it, cuda::std::true_type{});
 	if (qn) {
 		__syncwarp();
 		drain<NREG>(a, w, lane, 0, qn, rc.p, kmax);
@@ -319,7 +330,7 @@ __device__ __forceinline__ uint32_t row_loop(const SieveArgs& a, const WarpSmem&
 	// register-probe counts of this segment (per-row sums are < 2^32: 59p < 2^32)
 #pragma unroll
 	for (int j = 0; j < NREG; ++j) {
-		const uint32_t s = warp_sum(cnt[j]);
+		const uint32_t s = warp_sum(S[j] - S[j + 1]);
 		if (s) {
 			kmax = max(kmax, static_cast<uint32_t>(j + 1));
 			if (lane == 0) hist_add(a, w.hist, j, s);
