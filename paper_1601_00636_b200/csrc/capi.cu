@@ -671,6 +671,8 @@ int enqueue_sieve(cgpu_ctx* c, uint64_t p_lo, uint64_t q_start, uint64_t p_hi, i
 
 	SieveArgs a{};
 	a.ext = c->ext.p;
+	a.ext_words = c->ext_words;
+	a.n_blocks = nblocks;
 	a.probes = c->probes.p;
 	a.np = c->np;
 	a.nreg = c->nreg;

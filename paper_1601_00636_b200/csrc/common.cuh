@@ -4,6 +4,20 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+// Device-side bounds checks, compiled in only for the debug build
+// (make EXTRA=-DCGPU_DEBUG ...): a violated check traps the kernel, which the
+// host sees as a CUDA error. compute-sanitizer is unavailable on this pool.
+#ifdef CGPU_DEBUG
+#define CGPU_CHECK(cond)          \
+	do {                          \
+		if (!(cond)) __trap();    \
+	} while (0)
+#else
+#define CGPU_CHECK(cond) \
+	do {                 \
+	} while (0)
+#endif
+
 namespace cgpu {
 
 constexpr uint32_t kModulusLimit = 9697;      // primes.hpp:12

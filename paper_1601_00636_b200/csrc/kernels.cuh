@@ -64,6 +64,8 @@ constexpr uint32_t kPlanChunk = 1024;  // row slots per plan CTA
 
 struct SieveArgs {
 	const uint32_t* ext;          // row-extended tables
+	uint64_t ext_words;           // (debug bounds checks)
+	uint64_t n_blocks;            // block_rmax entries (debug bounds checks)
 	const uint4* probes;          // per probe j: {r, m, ext_base, S}
 	uint32_t np;                  // probes (killable tables, rank order)
 	uint32_t nreg;                // leading probes held in registers
@@ -95,7 +97,7 @@ struct SieveArgs {
 cudaError_t launch_plan(const SieveArgs& a, cudaStream_t s);
 cudaError_t launch_sieve(const SieveArgs& a, int grid, cudaStream_t s);
 int sieve_grid(int device, int nreg, size_t smem_bytes);
-size_t sieve_smem_bytes(uint32_t np);
+__host__ __device__ size_t sieve_smem_bytes(uint32_t np);
 __host__ __device__ inline uint32_t plan_chunks(uint32_t n_slots) { return (n_slots + kPlanChunk - 1) / kPlanChunk; }
 
 cudaError_t launch_init_blocks(uint32_t* d_block_rmax, uint64_t nblocks, uint64_t blk_lo,

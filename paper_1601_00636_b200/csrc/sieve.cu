@@ -160,6 +160,13 @@ __global__ void __launch_bounds__(kPlanChunk) k_plan(const SieveArgs a)
 	}
 }
 
+__device__ __forceinline__ uint32_t dynamic_smem_size()
+{
+	uint32_t v;
+	asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(v));
+	return v;
+}
+
 __device__ __forceinline__ uint32_t warp_sum(uint32_t v)
 {
 	return __reduce_add_sync(kFull, v);
@@ -225,6 +232,7 @@ __device__ __forceinline__ void drain(const SieveArgs& a, const WarpSmem& w, uin
 			const uint4 d = w.desc[j];
 			const uint32_t b = mod_full(q0, d.y, d.z);
 			const uint32_t* wp = a.ext + d.x + (b >> 5);
+			CGPU_CHECK(d.x + (b >> 5) + 1 < a.ext_words);
 			const uint32_t M = __funnelshift_r(__ldg(wp), __ldg(wp + 1), b);
 			const uint32_t k = alive & M;
 			alive ^= k;
@@ -275,6 +283,7 @@ __device__ __forceinline__ uint32_t row_loop(const SieveArgs& a, const WarpSmem&
 	for (int j = 0; j < NREG; ++j) {
 		const uint32_t r = a.reg_r[j], m = a.reg_m[j];
 		const uint32_t row = a.reg_base[j] + mod_full(rc.p, r, m) * 2;  // S = 2 for r <= 31
+		CGPU_CHECK(row + 1 < a.ext_words);
 		rw0[j] = __ldg(a.ext + row);
 		rw1[j] = __ldg(a.ext + row + 1);
 		rb[j] = mod_full(q0_first, r, m);
@@ -306,6 +315,7 @@ __device__ __forceinline__ uint32_t row_loop(const SieveArgs& a, const WarpSmem&
 		}
 		const uint32_t m = __ballot_sync(kFull, alive != 0);
 		if (m) {
+			CGPU_CHECK(qn + __popc(m) <= kQueue);
 			if (alive) w.queue[qn + __popc(m & lt)] = make_uint2(q0, alive);
 			qn += __popc(m);
 			if (qn >= 32) {
@@ -374,6 +384,7 @@ __global__ void __launch_bounds__(kSieveThreads, kSieveMinBlocks) k_sieve(const 
 	for (uint32_t j = lane; j < a.np; j += 32) w.hist[j] = 0;
 	__syncwarp();
 
+	CGPU_CHECK(sieve_smem_bytes(a.np) <= dynamic_smem_size());
 	const uint32_t n_chunks = plan_chunks(a.n_slots);
 	const unsigned long long W = a.chunk_off[n_chunks];
 	const unsigned long long nwarps = static_cast<unsigned long long>(gridDim.x) * kSieveWarps;
@@ -467,6 +478,7 @@ __global__ void __launch_bounds__(kSieveThreads, kSieveMinBlocks) k_sieve(const 
 		if (lane == 0 && kk) {
 			const uint32_t j = kk - 1;
 			const uint32_t killer = j < NREG ? a.reg_r[j < NREG ? j : 0] : w.desc[j].y;
+			CGPU_CHECK(rb.p / 100 - a.blk_lo < a.n_blocks);
 			atomicMax(&a.block_rmax[rb.p / 100 - a.blk_lo], killer);
 		}
 		__syncwarp();
@@ -554,7 +566,7 @@ void* sieve_kernel_ptr(int nreg)
 
 }  // namespace
 
-size_t sieve_smem_bytes(uint32_t np)
+__host__ __device__ size_t sieve_smem_bytes(uint32_t np)
 {
 	return (sizeof(uint4) + sizeof(uint32_t)) * static_cast<size_t>(np) * kSieveWarps +
 	       sizeof(uint2) * kQueue * kSieveWarps;
