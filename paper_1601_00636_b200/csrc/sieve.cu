@@ -297,12 +297,17 @@ __device__ __forceinline__ uint32_t row_loop(const SieveArgs& a, const WarpSmem&
 	uint32_t fo[NF > 0 ? NF : 1], fd[NF > 0 ? NF : 1], fpat[NF > 0 ? NF : 1], ff[NF > 0 ? NF : 1];
 #pragma unroll
 	for (int k = 0; k < NF; ++k) {
-		const uint32_t f = rc.fac[k];
-		const uint32_t b = q0_first % f;
-		ff[k] = f;
-		fo[k] = b ? f - b : 0;
-		fd[k] = kStepQ % f;
-		fpat[k] = period_mask(f);
+		if (k < static_cast<int>(rc.nf)) {
+			const uint32_t f = rc.fac[k];
+			const uint32_t b = q0_first % f;
+			ff[k] = f;
+			fo[k] = b ? f - b : 0;
+			fd[k] = kStepQ % f;
+			fpat[k] = period_mask(f);
+		} else {  // padding slot of a wider variant: contributes no bits
+			ff[k] = 1;
+			fo[k] = fd[k] = fpat[k] = 0;
+		}
 	}
 	uint32_t rw0[NREG > 0 ? NREG : 1], rw1[NREG > 0 ? NREG : 1], rb[NREG > 0 ? NREG : 1];
 #pragma unroll
@@ -356,7 +361,9 @@ __device__ __forceinline__ uint32_t row_loop(const SieveArgs& a, const WarpSmem&
 	const uint32_t E = min(rc.w1, rc.wlast);  // windows below E are whole and in the slice
 	const uint32_t n_full = E > rc.w0 ? min((E - rc.w0) / 32, n_iter) : 0;
 	uint32_t it = 0;
+#ifndef CGPU_NO_EDGE_SPEC
 	for (; it < n_full; ++it) step(it, cuda::std::false_type{});
+#endif
 	for (; it < n_iter; ++it) step(it, cuda::std::true_type{});
 	if (qn) {
 		__syncwarp();
@@ -386,16 +393,18 @@ template <int NREG>
 __device__ __forceinline__ uint32_t dispatch_row(const SieveArgs& a, const WarpSmem& w, uint32_t lane,
                                                  const RowCtx& rc)
 {
+	// Four variants, not ten: a row uses the narrowest one with enough factor
+	// slots (padding slots cost 4 instructions per window). Fewer copies of
+	// the loop keep the kernel in the instruction cache when consecutive rows
+	// differ in their factor count (C5: 60% of the work has <= 2 odd factors,
+	// 32% has 3, 8% has 4-5).
 	switch (rc.nf) {
-	case 0: return row_loop<NREG, 0>(a, w, lane, rc);
-	case 1: return row_loop<NREG, 1>(a, w, lane, rc);
+	case 0:
+	case 1:
 	case 2: return row_loop<NREG, 2>(a, w, lane, rc);
 	case 3: return row_loop<NREG, 3>(a, w, lane, rc);
-	case 4: return row_loop<NREG, 4>(a, w, lane, rc);
+	case 4:
 	case 5: return row_loop<NREG, 5>(a, w, lane, rc);
-	case 6: return row_loop<NREG, 6>(a, w, lane, rc);
-	case 7: return row_loop<NREG, 7>(a, w, lane, rc);
-	case 8: return row_loop<NREG, 8>(a, w, lane, rc);
 	default: return row_loop<NREG, 9>(a, w, lane, rc);
 	}
 }
