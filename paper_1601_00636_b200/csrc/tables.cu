@@ -69,19 +69,27 @@ __device__ __forceinline__ void store_word_bytes(uint8_t* table, uint32_t tbytes
 // consecutive bits of the reference's global index) and evaluates
 //     Q = s^5 + c4 s^4 + c3 s^3 + c2 s^2 + c1 s + c0   (s = t^2, modpoly.hpp:3-11)
 // at every t. The powers s^k mod r depend only on t, so they are tabulated
-// once per CTA in shared memory and read as broadcasts; the evaluation is then
-// four IMADs into an accumulator < 4r^2 + r < 2^24 and ONE Barrett reduction,
-// compared against -c0 mod r (the lazy remainder lies in [0, 2r)). Same value
-// as the reference's Horner (modpoly.hpp:116-125), half the multiplies.
+// once per CTA in shared memory and read as broadcasts; per evaluation that
+// leaves four IMADs into an accumulator A = c0 + c1 s + ... + c4 s^4 < 2^24
+// and ONE more IMAD for the test: for odd r, r | x iff x * r^-1 (mod 2^32) <=
+// (2^32 - 1) / r (divisibility by multiplicative inverse), and
+// (A + s^5) r^-1 = A r^-1 + (s^5 r^-1) with the second term tabulated per t.
+// A running minimum over t decides the bit. Same value as the reference's
+// Horner (modpoly.hpp:116-125) with no reduction at all in the loop.
 __global__ void __launch_bounds__(kCubeThreads) k_cube(const PrimeJob* __restrict__ jobs,
                                                        uint8_t* __restrict__ packed)
 {
-	extern __shared__ uint4 s_pw[];  // [r] {s, s^2, s^3, s^4} then [r] s^5
+	extern __shared__ uint4 s_pw[];  // [r] {s, s^2, s^3, s^4} then [r] s^5 r^-1 mod 2^32
 	const PrimeJob job = jobs[blockIdx.y];
 	const uint32_t r = job.r, m = job.m;
 	const uint32_t rr = r * r;
 	const uint32_t per_cta = kCubeThreads * kCubePairs;
 	if (blockIdx.x * per_cta >= rr) return;
+	// r^-1 mod 2^32 by Newton iteration (r odd); r = 2 uses the Barrett test
+	uint32_t rinv = r;
+	for (int i = 0; i < 5; ++i) rinv *= 2u - r * rinv;
+	const bool odd = r & 1;
+	const uint32_t lim = 0xffffffffu / r;
 	uint32_t* s_p5 = reinterpret_cast<uint32_t*>(s_pw + r);
 	for (uint32_t t = threadIdx.x; t < r; t += blockDim.x) {
 		const uint32_t s1 = mod_full(t * t, r, m);
@@ -89,16 +97,14 @@ __global__ void __launch_bounds__(kCubeThreads) k_cube(const PrimeJob* __restric
 		const uint32_t s3 = mod_full(s2 * s1, r, m);
 		const uint32_t s4 = mod_full(s3 * s1, r, m);
 		s_pw[t] = make_uint4(s1, s2, s3, s4);
-		s_p5[t] = mod_full(s4 * s1, r, m);
+		s_p5[t] = mod_full(s4 * s1, r, m) * (odd ? rinv : 1u);
 	}
 	__syncthreads();
 	const uint32_t tbytes = (rr + 7) >> 3;
 	const uint32_t lane = threadIdx.x & 31;
-	uint32_t nr;  // x - q r as one IMAD x + q * (2^32 - r); opaque so it is not re-negated
-	asm("mov.b32 %0, %1;" : "=r"(nr) : "r"(0u - r));
 	for (uint32_t base = blockIdx.x * per_cta; base < rr; base += gridDim.x * per_cta) {
-		uint32_t c1[kCubePairs], c2[kCubePairs], c3[kCubePairs], c4[kCubePairs], nz[kCubePairs];
-		uint32_t mn[kCubePairs];  // min over t of (Q mod r) - (-c0): 0 iff some t is a root
+		uint32_t c0[kCubePairs], c1[kCubePairs], c2[kCubePairs], c3[kCubePairs], c4[kCubePairs];
+		uint32_t mn[kCubePairs];  // min over t of (Q r^-1 mod 2^32): a root iff <= lim
 		bool valid[kCubePairs];
 #pragma unroll
 		for (int k = 0; k < kCubePairs; ++k) {
@@ -112,26 +118,37 @@ __global__ void __launch_bounds__(kCubeThreads) k_cube(const PrimeJob* __restric
 			c3[k] = c[1];
 			c2[k] = c[2];
 			c1[k] = c[3];
-			nz[k] = 0u - (c[4] ? r - c[4] : 0);  // Q == 0 <=> s^5 + ... + c1 s == -c0 (mod r)
+			c0[k] = c[4];
 			mn[k] = 0xffffffffu;
 		}
+		if (odd) {
 #pragma unroll 2
-		for (uint32_t t = 0; t < r; ++t) {
-			const uint4 p = s_pw[t];
-			const uint32_t p5 = s_p5[t];
+			for (uint32_t t = 0; t < r; ++t) {
+				const uint4 p = s_pw[t];
+				const uint32_t p5 = s_p5[t];
 #pragma unroll
-			for (int k = 0; k < kCubePairs; ++k) {
-				uint32_t acc = c4[k] * p.w + p5;
-				acc = c3[k] * p.z + acc;
-				acc = c2[k] * p.y + acc;
-				acc = c1[k] * p.x + acc;
-				const uint32_t x = acc + __umulhi(acc, m) * nr;  // [0, 2r)
-				mn[k] = min(min(x, x - r) + nz[k], mn[k]);       // two VIADDMNMX
+				for (int k = 0; k < kCubePairs; ++k) {
+					uint32_t acc = c4[k] * p.w + c0[k];
+					acc = c3[k] * p.z + acc;
+					acc = c2[k] * p.y + acc;
+					acc = c1[k] * p.x + acc;                  // < 4r^2 + r < 2^24
+					mn[k] = min(mn[k], acc * rinv + p5);       // (A + s^5) r^-1 mod 2^32
+				}
+			}
+		} else {  // r = 2: remainder by Barrett, shifted so that 0 means a root
+			for (uint32_t t = 0; t < r; ++t) {
+				const uint4 p = s_pw[t];
+				const uint32_t p5 = s_p5[t];
+#pragma unroll
+				for (int k = 0; k < kCubePairs; ++k) {
+					const uint32_t acc = c4[k] * p.w + c3[k] * p.z + c2[k] * p.y + c1[k] * p.x + c0[k] + p5;
+					mn[k] = min(mn[k], mod_full(acc, r, m) ? lim + 1 : 0u);
+				}
 			}
 		}
 #pragma unroll
 		for (int k = 0; k < kCubePairs; ++k) {
-			const uint32_t word = __ballot_sync(kFull, valid[k] && mn[k] != 0);
+			const uint32_t word = __ballot_sync(kFull, valid[k] && mn[k] > lim);
 			const uint32_t i0 = base + k * kCubeThreads + (threadIdx.x & ~31u);
 			store_word_bytes(packed + job.byte_off, tbytes, i0, word, lane);
 		}
