@@ -153,7 +153,7 @@ class CpuReference:
         self.wl, self.primes = wl, primes
         span = wl["p_hi"] - wl["p_lo"] + 1
         self.span = span
-        self.p0 = wl["p_lo"] + (SEED % max(span - 20000, 1))
+        self.p0 = wl["p_lo"] + (SEED % max(span - 40000, 1))
         if refmod.available():
             rs = refmod.RefSet.build(primes)
             self._run = lambda lo, hi: refmod.triangle(rs, lo, hi, threads, with_sink=False).pairs_tested
@@ -168,7 +168,7 @@ class CpuReference:
         self.sec_per_row = max(time.perf_counter() - t, 1e-4) / 200
 
     def sample(self, budget_s):
-        rows = int(min(max(budget_s / self.sec_per_row, 20), min(self.span, 20000)))
+        rows = int(min(max(budget_s / self.sec_per_row, 20), self.wl["p_hi"] - self.p0 + 1, 40000))
         t = time.perf_counter()
         pairs = self._run(self.p0, self.p0 + rows - 1)
         return dict(pairs=pairs, seconds=time.perf_counter() - t, rows=(self.p0, self.p0 + rows - 1),
