@@ -221,8 +221,9 @@ __global__ void __launch_bounds__(kPermThreads) k_permute(const PrimeJob* __rest
 }
 
 // Packed reference tables -> row-extended words (common.cuh ext_row_words):
-// word j of row a holds bits u(a, (32j + l) mod r), l = 0..31. One warp per
-// word; killable[k] is set when any word of table k is nonzero.
+// word j of row a holds bits u(a, (32j + l) mod r), l = 0..31. One thread per
+// word gathers its 32 bits from the packed row (L1-resident bytes);
+// killable[k] is set when any word of table k is nonzero.
 __global__ void __launch_bounds__(kDeriveThreads) k_derive(const PrimeJob* __restrict__ jobs,
                                                            const uint8_t* __restrict__ packed,
                                                            uint32_t* __restrict__ ext,
@@ -231,20 +232,25 @@ __global__ void __launch_bounds__(kDeriveThreads) k_derive(const PrimeJob* __res
 	const PrimeJob job = jobs[blockIdx.y];
 	const uint32_t r = job.r, m = job.m, S = ext_row_words(r);
 	const uint32_t words = r * S;
-	const uint32_t lane = threadIdx.x & 31;
-	const uint32_t wpb = blockDim.x / 32;
 	const uint8_t* tab = packed + job.byte_off;
+	const uint32_t mS = barrett_m(S);
 	bool any = false;
-	for (uint32_t w = blockIdx.x * wpb + threadIdx.x / 32; w < words; w += gridDim.x * wpb) {
-		const uint32_t a = w / S, j = w - a * S;
-		const uint32_t q = mod_full(32 * j + lane, r, m);
-		const uint32_t idx = a * r + q;
-		const uint32_t bit = (__ldg(tab + (idx >> 3)) >> (idx & 7)) & 1u;
-		const uint32_t word = __ballot_sync(kFull, bit);
-		if (lane == 0) ext[job.ext_base + w] = word;
+	for (uint32_t w = blockIdx.x * blockDim.x + threadIdx.x; w < words; w += gridDim.x * blockDim.x) {
+		uint32_t a = __umulhi(w, mS), j = w - a * S;  // w / S, w % S
+		if (j >= S) { j -= S; ++a; }
+		uint32_t b = mod_full(32 * j, r, m);  // offset of bit 0 of the word in the row
+		const uint32_t row0 = a * r;
+		uint32_t word = 0;
+#pragma unroll 8
+		for (uint32_t l = 0; l < 32; ++l) {
+			const uint32_t idx = row0 + b;
+			word |= ((__ldg(tab + (idx >> 3)) >> (idx & 7)) & 1u) << l;
+			b = b + 1 == r ? 0 : b + 1;
+		}
+		ext[job.ext_base + w] = word;
 		any |= word != 0;
 	}
-	if (lane == 0 && any) atomicOr(&killable[blockIdx.y], 1u);
+	if (__any_sync(kFull, any) && (threadIdx.x & 31) == 0) atomicOr(&killable[blockIdx.y], 1u);
 }
 
 // FormatError check (sievetable.hpp:67-79): bits >= r^2 of the last byte of
@@ -310,7 +316,7 @@ cudaError_t launch_derive(const PrimeJob* d_jobs, uint32_t njobs, uint64_t max_w
                           cudaStream_t s)
 {
 	if (!njobs) return cudaSuccess;
-	const dim3 grid(grid_x(max_words, kDeriveThreads / 32, 256), njobs);
+	const dim3 grid(grid_x(max_words, kDeriveThreads, 1024), njobs);
 	k_derive<<<grid, kDeriveThreads, 0, s>>>(d_jobs, d_packed, d_ext, d_killable);
 	return cudaGetLastError();
 }
