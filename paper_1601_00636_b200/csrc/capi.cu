@@ -149,7 +149,7 @@ struct cgpu_ctx {
 
 	// sieve buffers
 	DevBuf<unsigned long long> hist, counters, surv, prefix, chunk_off;
-	DevBuf<uint32_t> tickets;
+	DevBuf<uint32_t> tickets, rowfac;
 	DevBuf<uint32_t> d_probe_rank;
 	DevBuf<uint32_t> block_rmax;
 	bool launched = false, results_internal = false, timed = false;
@@ -708,6 +708,8 @@ int enqueue_sieve(cgpu_ctx* c, uint64_t p_lo, uint64_t q_start, uint64_t p_hi, i
 		CK(c->prefix.ensure(max_slots + 1));
 		CK(c->chunk_off.ensure(plan_chunks(static_cast<uint32_t>(max_slots)) + 1));
 		CK(c->tickets.ensure(2));
+		CK(c->rowfac.ensure(max_slots * kFacWords));
+		a.rowfac = c->rowfac.p;
 		CK(cudaMemsetAsync(c->tickets.p, 0, 8, c->stream));
 		a.prefix = c->prefix.p;
 		a.chunk_off = c->chunk_off.p;

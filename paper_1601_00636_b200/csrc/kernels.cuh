@@ -61,6 +61,7 @@ constexpr int kMaxReg = 8;      // leading probes held in registers (r <= 31)
 constexpr int kMaxFactors = 9;  // distinct prime factors of p < 2^32
 constexpr int kQueue = 64;      // per-warp deep-probe work queue entries
 constexpr uint32_t kPlanChunk = 1024;  // row slots per plan CTA
+constexpr uint32_t kFacWords = 1 + kMaxFactors;  // per row slot: nf | even << 8, odd factors
 
 struct SieveArgs {
 	const uint32_t* ext;          // row-extended tables
@@ -83,6 +84,7 @@ struct SieveArgs {
 	unsigned long long* prefix;        // [n_slots + 1] (chunk-local exclusive scan)
 	unsigned long long* chunk_off;     // [n_chunks + 1] (exclusive scan of chunk totals)
 	uint32_t* tickets;                 // [2] last-CTA tickets (plan, sieve), zeroed per launch
+	uint32_t* rowfac;                  // [n_slots][kFacWords] row factorisations (k_plan)
 	// outputs
 	unsigned long long* hist;          // [n primes] first-killer counts by rank
 	uint32_t nprimes;

@@ -128,6 +128,40 @@ __device__ __forceinline__ unsigned long long block_excl_scan(unsigned long long
 	return x - v + (wid ? s_warp[wid - 1] : 0);
 }
 
+// Distinct prime factors of row p for the sieve's coprimality masks (trial
+// division by the primes below 2^16 with Barrett remainders): out[0] =
+// nf | even << 8, out[1..nf] = the odd prime factors that can divide some q of
+// the row (<= qhi). Empty rows get nf = 0.
+__device__ __forceinline__ void factorise(const SieveArgs& a, const RowBounds& rb, uint32_t* out)
+{
+	uint32_t nf = 0, even = 0;
+	if (rb.qhi >= rb.qlo) {
+		const uint32_t p = static_cast<uint32_t>(rb.p);
+		const uint64_t qhi = rb.qhi;
+		uint32_t cof = p;
+		for (uint32_t i = 0; i < a.n_fprimes; ++i) {
+			const uint2 fp = __ldg(a.fprimes + i);
+			if (static_cast<uint64_t>(fp.x) * fp.x > cof) break;
+			uint32_t qt = __umulhi(cof, fp.y), rem = cof - qt * fp.x;
+			if (rem >= fp.x) { rem -= fp.x; ++qt; }
+			if (rem) continue;
+			if (fp.x == 2) even = 1;
+			else if (fp.x <= qhi && nf < kMaxFactors) out[1 + nf++] = fp.x;
+			do {  // divide f out of the cofactor
+				cof = qt;
+				qt = __umulhi(cof, fp.y);
+				rem = cof - qt * fp.x;
+				if (rem >= fp.x) { rem -= fp.x; ++qt; }
+			} while (!rem);
+		}
+		if (cof > 1) {  // the prime factor above sqrt of the remaining cofactor
+			if (cof == 2) even = 1;
+			else if (cof <= qhi && nf < kMaxFactors) out[1 + nf++] = cof;
+		}
+	}
+	out[0] = nf | (even << 8);
+}
+
 // Plan: per row slot, the work units before it. Each CTA scans kPlanChunk
 // slots; the last CTA to finish scans the chunk totals.
 __global__ void __launch_bounds__(kPlanChunk) k_plan(const SieveArgs a)
@@ -136,7 +170,9 @@ __global__ void __launch_bounds__(kPlanChunk) k_plan(const SieveArgs a)
 	__shared__ bool s_last;
 	const uint32_t n = a.n_slots;
 	const uint32_t s = blockIdx.x * kPlanChunk + threadIdx.x;
-	const unsigned long long u = s < n ? row_units(a, slot_row(a, s)) : 0;
+	const RowBounds rb = s < n ? slot_row(a, s) : RowBounds{0, 1, 0};
+	const unsigned long long u = s < n ? row_units(a, rb) : 0;
+	if (s < n) factorise(a, rb, a.rowfac + static_cast<size_t>(s) * kFacWords);
 	unsigned long long total;
 	const unsigned long long ex = block_excl_scan(u, s_warp, total);
 	if (s < n) a.prefix[s] = ex;
@@ -183,7 +219,6 @@ __device__ __forceinline__ void hist_add(const SieveArgs& a, uint32_t* h, uint32
 }
 
 struct WarpSmem {
-	uint4* desc;     // [np] per deep probe: {row word base, r, m, -} for the current row
 	uint2* queue;    // [kQueue] windows alive after the register probes: {q0, alive}
 	uint32_t* hist;  // [np] first-kill counts of this warp
 };
@@ -231,10 +266,12 @@ __device__ __forceinline__ uint32_t drain(const SieveArgs& a, const WarpSmem& w,
 		if (!__any_sync(kFull, alive)) break;
 		uint32_t c = 0;
 		if (alive) {
-			const uint4 d = w.desc[j];
-			const uint32_t b = mod_full(q0, d.y, d.z);
-			const uint32_t* wp = a.ext + d.x + (b >> 5);
-			CGPU_CHECK(d.x + (b >> 5) + 1 < a.ext_words);
+			// probe j = {r, m, ext_base, S}; row p mod r of its ext table
+			const uint4 d = __ldg(a.probes + j);
+			const uint32_t row = d.z + mod_full(p, d.x, d.y) * d.w;
+			const uint32_t b = mod_full(q0, d.x, d.y);
+			const uint32_t* wp = a.ext + row + (b >> 5);
+			CGPU_CHECK(row + (b >> 5) + 1 < a.ext_words);
 			const uint32_t M = __funnelshift_r(__ldg(wp), __ldg(wp + 1), b);
 			const uint32_t k = alive & M;
 			alive ^= k;
@@ -418,8 +455,7 @@ __global__ void __launch_bounds__(kSieveThreads, kSieveMinBlocks) k_sieve(const 
 	const uint32_t lane = threadIdx.x & 31;
 	const uint32_t wib = threadIdx.x >> 5;
 	WarpSmem w;
-	w.desc = s_dyn + static_cast<size_t>(wib) * a.np;
-	uint2* q_all = reinterpret_cast<uint2*>(s_dyn + static_cast<size_t>(kSieveWarps) * a.np);
+	uint2* q_all = reinterpret_cast<uint2*>(s_dyn);
 	w.queue = q_all + wib * kQueue;
 	uint32_t* h_all = reinterpret_cast<uint32_t*>(q_all + kSieveWarps * kQueue);
 	w.hist = h_all + static_cast<size_t>(wib) * a.np;
@@ -472,55 +508,23 @@ __global__ void __launch_bounds__(kSieveThreads, kSieveMinBlocks) k_sieve(const 
 		rc.wlast = (qhi - rc.qlo) / 32;
 		rc.tail = (2u << (qhi - (rc.qlo + 32 * rc.wlast))) - 1;  // span 31 -> all ones
 
-		// ---- distinct prime factors of p (trial division, warp-parallel) ----
+		// ---- distinct prime factors of p, factorised by k_plan ----
 		// f = 2 becomes a constant mask (the q step per lane is even); odd
-		// factors above qhi cannot divide any q of the row and are dropped.
-		rc.nf = 0;
-		bool even = false;
-		{
-			uint32_t cof = rc.p;
-			for (uint32_t base = 0; base < a.n_fprimes; base += 32) {
-				const uint32_t i = base + lane;
-				uint2 fp = make_uint2(0xffffffffu, 0);
-				if (i < a.n_fprimes) fp = __ldg(a.fprimes + i);
-				const bool in_range = i < a.n_fprimes && static_cast<uint64_t>(fp.x) * fp.x <= rc.p;
-				const bool divides = in_range && mod_full(rc.p, fp.x, fp.y) == 0;
-				uint32_t hits = __ballot_sync(kFull, divides);
-				while (hits) {
-					const uint32_t src = __ffs(hits) - 1;
-					hits &= hits - 1;
-					const uint32_t f = __shfl_sync(kFull, fp.x, src);
-					const uint32_t fm = __shfl_sync(kFull, fp.y, src);
-					if (f == 2) even = true;
-					else if (f <= qhi && rc.nf < kMaxFactors) rc.fac[rc.nf++] = f;
-					for (;;) {  // divide f out of the cofactor
-						const uint32_t qt = __umulhi(cof, fm);
-						uint32_t rem = cof - qt * f, qq = qt;
-						if (rem >= f) { rem -= f; ++qq; }
-						if (rem) break;
-						cof = qq;
-					}
-				}
-				if (!__any_sync(kFull, in_range)) break;
-			}
-			// the prime factor above sqrt(p), if any
-			if (cof > 1 && cof <= qhi && rc.nf < kMaxFactors) rc.fac[rc.nf++] = cof;
-		}
+		// factors above qhi cannot divide any q of the row and were dropped.
+		const uint32_t fw = lane < kFacWords ? __ldg(a.rowfac + static_cast<size_t>(cur) * kFacWords + lane) : 0u;
+		const uint32_t head = __shfl_sync(kFull, fw, 0);
+		rc.nf = head & 0xffu;
+		const bool even = (head >> 8) & 1u;
+#pragma unroll
+		for (int k = 0; k < kMaxFactors; ++k) rc.fac[k] = __shfl_sync(kFull, fw, k + 1);
 		// q0 parity is fixed per lane (q advances by 32 per window): even p
 		// excludes the even q of every window
 		rc.even = even ? (((rc.qlo + 32 * (rc.w0 + lane)) & 1) ? 0xAAAAAAAAu : 0x55555555u) : 0u;
 
-		// ---- deep probe descriptors for this row (rank order) ----
-		for (uint32_t j = NREG + lane; j < a.np; j += 32) {
-			const uint4 d = __ldg(a.probes + j);
-			w.desc[j] = make_uint4(d.z + mod_full(rc.p, d.x, d.y) * d.w, d.x, d.y, 0);
-		}
-		__syncwarp();
-
 		const uint32_t kk = dispatch_row<NREG>(a, w, lane, rc);  // 1 + deepest killer
 		if (lane == 0 && kk) {
 			const uint32_t j = kk - 1;
-			const uint32_t killer = j < NREG ? a.reg_r[j < NREG ? j : 0] : w.desc[j].y;
+			const uint32_t killer = j < NREG ? a.reg_r[j < NREG ? j : 0] : __ldg(a.probes + j).x;
 			CGPU_CHECK(rb.p / 100 - a.blk_lo < a.n_blocks);
 			atomicMax(&a.block_rmax[rb.p / 100 - a.blk_lo], killer);
 		}
@@ -611,8 +615,7 @@ void* sieve_kernel_ptr(int nreg)
 
 __host__ __device__ size_t sieve_smem_bytes(uint32_t np)
 {
-	return (sizeof(uint4) + sizeof(uint32_t)) * static_cast<size_t>(np) * kSieveWarps +
-	       sizeof(uint2) * kQueue * kSieveWarps;
+	return sizeof(uint32_t) * static_cast<size_t>(np) * kSieveWarps + sizeof(uint2) * kQueue * kSieveWarps;
 }
 
 int sieve_grid(int device, int nreg, size_t smem)
