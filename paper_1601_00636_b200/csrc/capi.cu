@@ -137,11 +137,11 @@ struct cgpu_ctx {
 	DevBuf<PrimeJob> jobs_rank;
 
 	// probe list
-	uint32_t np = 0, nreg = 0;
+	uint32_t np = 0, nreg = 0, nreg2 = 0, nreg3 = 0;
 	std::vector<uint32_t> probe_rank, probe_r;
 	DevBuf<uint4> probes;
 	uint32_t reg_r[kMaxReg] = {}, reg_m[kMaxReg] = {}, reg_base[kMaxReg] = {}, reg_delta[kMaxReg] = {};
-	int grid[kMaxReg + 1] = {};
+	int grid = 0;
 
 	uint32_t row_cost = kDefaultRowCost;
 	DevBuf<uint2> fprimes;
@@ -329,14 +329,28 @@ int finalize_set(cgpu_ctx* c)
 		pr.push_back(make_uint4(r, barrett_m(r), c->ext_base[k], ext_row_words(r)));
 	}
 	c->np = static_cast<uint32_t>(pr.size());
-	c->nreg = 0;
-	while (c->nreg < c->np && c->nreg < static_cast<uint32_t>(kMaxReg) && c->probe_r[c->nreg] <= 31) {
-		const uint32_t j = c->nreg, r = c->probe_r[j];
+	// register probes: the leading killable primes <= 31 (two-word rows), then,
+	// when all of 11..31 are among them, up to kMaxReg3 primes in (31, 63]
+	c->nreg = c->nreg2 = c->nreg3 = 0;
+	uint32_t cap2 = kMaxReg2, cap3 = 1;  // measured: one 3-word probe (r = 37) is best
+	if (const char* e = std::getenv("CUBOID_MAX_REG_PROBES")) cap2 = std::min<uint32_t>(cap2, std::atoi(e));
+	if (const char* e = std::getenv("CUBOID_REG3_PROBES")) cap3 = std::min<uint32_t>(kMaxReg3, std::atoi(e));
+	auto add_reg = [&](uint32_t j) {
+		const uint32_t r = c->probe_r[j];
 		c->reg_r[j] = r;
 		c->reg_m[j] = barrett_m(r);
 		c->reg_base[j] = pr[j].z;
 		c->reg_delta[j] = (32u * 32u) % r;
 		++c->nreg;
+	};
+	while (c->nreg < c->np && c->nreg2 < cap2 && c->probe_r[c->nreg] <= 31) {
+		add_reg(c->nreg);
+		++c->nreg2;
+	}
+	const bool all_small = c->nreg2 == 7 && c->probe_r[0] == 11 && c->probe_r[6] == 31;
+	while (all_small && c->nreg < c->np && c->nreg3 < cap3 && c->probe_r[c->nreg] <= 63) {
+		add_reg(c->nreg);
+		++c->nreg3;
 	}
 	CK(c->probes.ensure(c->np));
 	CK(c->d_probe_rank.ensure(c->np));
@@ -350,7 +364,7 @@ int finalize_set(cgpu_ctx* c)
 	const size_t smem = sieve_smem_bytes(c->np);
 	if (smem > 220 * 1024)
 		return set_err(CGPU_ERR_INVALID, "too many probe primes for the sieve's shared memory");
-	c->grid[c->nreg] = sieve_grid(c->device, static_cast<int>(c->nreg), smem);
+	c->grid = sieve_grid(c->device, static_cast<int>(c->nreg2), static_cast<int>(c->nreg3), smem);
 	CK(cudaGetLastError());
 	CK(cudaStreamSynchronize(c->stream));
 	c->loaded = true;
@@ -676,6 +690,8 @@ int enqueue_sieve(cgpu_ctx* c, uint64_t p_lo, uint64_t q_start, uint64_t p_hi, i
 	a.probes = c->probes.p;
 	a.np = c->np;
 	a.nreg = c->nreg;
+	a.nreg2 = c->nreg2;
+	a.nreg3 = c->nreg3;
 	for (int j = 0; j < kMaxReg; ++j) {
 		a.reg_r[j] = c->reg_r[j];
 		a.reg_m[j] = c->reg_m[j];
@@ -721,7 +737,7 @@ int enqueue_sieve(cgpu_ctx* c, uint64_t p_lo, uint64_t q_start, uint64_t p_hi, i
 			CK(launch_plan(a, c->stream));
 			if (!ev1) CK(cudaEventRecord(c->ev[1], c->stream));  // sieve time excludes the first plan
 			ev1 = true;
-			CK(launch_sieve(a, c->grid[c->nreg], c->stream));
+			CK(launch_sieve(a, c->grid, c->stream));
 			c->launches += 2;
 		}
 	}

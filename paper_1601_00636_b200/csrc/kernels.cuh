@@ -57,7 +57,9 @@ constexpr int kSieveThreads = 256;
 constexpr int kSieveMinBlocks = CGPU_SIEVE_MIN_BLOCKS;  // CTAs per SM the register budget targets
 constexpr uint32_t kDefaultRowCost = 600;                 // window-equivalents per row setup
 constexpr int kSieveWarps = kSieveThreads / 32;
-constexpr int kMaxReg = 8;      // leading probes held in registers (r <= 31)
+constexpr int kMaxReg2 = 8;     // leading probes held in registers with r <= 31 (2-word rows)
+constexpr int kMaxReg3 = 4;     // then with 31 < r <= 63 (3-word rows), after all of 11..31
+constexpr int kMaxReg = kMaxReg2 + kMaxReg3;
 constexpr int kMaxFactors = 9;  // distinct prime factors of p < 2^32
 constexpr int kQueue = 64;      // per-warp deep-probe work queue entries
 constexpr uint32_t kPlanChunk = 1024;  // row slots per plan CTA
@@ -69,7 +71,8 @@ struct SieveArgs {
 	uint64_t n_blocks;            // block_rmax entries (debug bounds checks)
 	const uint4* probes;          // per probe j: {r, m, ext_base, S}
 	uint32_t np;                  // probes (killable tables, rank order)
-	uint32_t nreg;                // leading probes held in registers
+	uint32_t nreg;                // leading probes held in registers (nreg2 + nreg3)
+	uint32_t nreg2, nreg3;
 	uint32_t reg_r[kMaxReg], reg_m[kMaxReg], reg_base[kMaxReg], reg_delta[kMaxReg];
 	const uint2* fprimes;         // {f, barrett m} primes < 2^16 for trial division
 	uint32_t n_fprimes;
@@ -98,7 +101,7 @@ struct SieveArgs {
 
 cudaError_t launch_plan(const SieveArgs& a, cudaStream_t s);
 cudaError_t launch_sieve(const SieveArgs& a, int grid, cudaStream_t s);
-int sieve_grid(int device, int nreg, size_t smem_bytes);
+int sieve_grid(int device, int nr2, int nr3, size_t smem_bytes);
 __host__ __device__ size_t sieve_smem_bytes(uint32_t np);
 __host__ __device__ inline uint32_t plan_chunks(uint32_t n_slots) { return (n_slots + kPlanChunk - 1) / kPlanChunk; }
 

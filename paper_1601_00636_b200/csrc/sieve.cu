@@ -317,10 +317,11 @@ __device__ __forceinline__ uint32_t coprime_in(const RowCtx& rc, uint32_t lane, 
 // The window loop of one row segment, specialised on the number of odd prime
 // factors NF so the coprimality masks cost exactly NF x 4 instructions.
 // Returns 1 + the deepest probe that killed in this segment (0: none).
-template <int NREG, int NF>
+template <int NR2, int NR3, int NF>
 __device__ __forceinline__ uint32_t row_loop(const SieveArgs& a, const WarpSmem& w, uint32_t lane,
                                              const RowCtx& rc)
 {
+	constexpr int NREG = NR2 + NR3;  // register probes: NR2 with r <= 31, NR3 with 31 < r <= 63
 	// S[j] = sum over this lane's windows of popc(alive before register probe j);
 	// probe j's first-kill count is S[j] - S[j+1] (telescoping: one LOP3 per
 	// probe). S[0] (the candidates) is counted once per segment by
@@ -346,14 +347,18 @@ __device__ __forceinline__ uint32_t row_loop(const SieveArgs& a, const WarpSmem&
 			fo[k] = fd[k] = fpat[k] = 0;
 		}
 	}
+	// a row of r <= 31 is 2 words (64 bits >= r + 31), of 31 < r <= 63 three
 	uint32_t rw0[NREG > 0 ? NREG : 1], rw1[NREG > 0 ? NREG : 1], rb[NREG > 0 ? NREG : 1];
+	uint32_t rw2[NR3 > 0 ? NR3 : 1];
 #pragma unroll
 	for (int j = 0; j < NREG; ++j) {
 		const uint32_t r = a.reg_r[j], m = a.reg_m[j];
-		const uint32_t row = a.reg_base[j] + mod_full(rc.p, r, m) * 2;  // S = 2 for r <= 31
-		CGPU_CHECK(row + 1 < a.ext_words);
+		const uint32_t S = j < NR2 ? 2 : 3;
+		const uint32_t row = a.reg_base[j] + mod_full(rc.p, r, m) * S;
+		CGPU_CHECK(row + S - 1 < a.ext_words);
 		rw0[j] = __ldg(a.ext + row);
 		rw1[j] = __ldg(a.ext + row + 1);
+		if (j >= NR2) rw2[j >= NR2 ? j - NR2 : 0] = __ldg(a.ext + row + 2);
 		rb[j] = mod_full(q0_first, r, m);
 	}
 	const uint32_t lt = (1u << lane) - 1;
@@ -375,7 +380,12 @@ __device__ __forceinline__ uint32_t row_loop(const SieveArgs& a, const WarpSmem&
 		if constexpr (decltype(edge)::value) alive &= wi < rc.w1 ? (wi < rc.wlast ? kFull : rc.tail) : 0u;
 #pragma unroll
 		for (int j = 0; j < NREG; ++j) {
-			alive &= ~__funnelshift_r(rw0[j], rw1[j], rb[j]);
+			if (j < NR2) {
+				alive &= ~__funnelshift_r(rw0[j], rw1[j], rb[j]);
+			} else {  // offset b in [0, 63): words (0,1) below 32, (1,2) above
+				const bool lo = rb[j] < 32;
+				alive &= ~__funnelshift_r(lo ? rw0[j] : rw1[j], lo ? rw1[j] : rw2[j >= NR2 ? j - NR2 : 0], rb[j]);
+			}
 			if (j + 1 < NREG) S[j + 1] += __popc(alive);
 			const uint32_t t = rb[j] + a.reg_delta[j];
 			rb[j] = min(t, t - a.reg_r[j]);
@@ -426,7 +436,7 @@ __device__ __forceinline__ uint32_t row_loop(const SieveArgs& a, const WarpSmem&
 	return kmax;
 }
 
-template <int NREG>
+template <int NR2, int NR3>
 __device__ __forceinline__ uint32_t dispatch_row(const SieveArgs& a, const WarpSmem& w, uint32_t lane,
                                                  const RowCtx& rc)
 {
@@ -438,17 +448,18 @@ __device__ __forceinline__ uint32_t dispatch_row(const SieveArgs& a, const WarpS
 	switch (rc.nf) {
 	case 0:
 	case 1:
-	case 2: return row_loop<NREG, 2>(a, w, lane, rc);
-	case 3: return row_loop<NREG, 3>(a, w, lane, rc);
+	case 2: return row_loop<NR2, NR3, 2>(a, w, lane, rc);
+	case 3: return row_loop<NR2, NR3, 3>(a, w, lane, rc);
 	case 4:
-	case 5: return row_loop<NREG, 5>(a, w, lane, rc);
-	default: return row_loop<NREG, 9>(a, w, lane, rc);
+	case 5: return row_loop<NR2, NR3, 5>(a, w, lane, rc);
+	default: return row_loop<NR2, NR3, 9>(a, w, lane, rc);
 	}
 }
 
-template <int NREG>
+template <int NR2, int NR3>
 __global__ void __launch_bounds__(kSieveThreads, kSieveMinBlocks) k_sieve(const SieveArgs a)
 {
+	constexpr int NREG = NR2 + NR3;
 	extern __shared__ uint4 s_dyn[];
 	__shared__ bool s_last;
 	__shared__ unsigned long long s_red[kSieveWarps];
@@ -521,7 +532,7 @@ __global__ void __launch_bounds__(kSieveThreads, kSieveMinBlocks) k_sieve(const 
 		// excludes the even q of every window
 		rc.even = even ? (((rc.qlo + 32 * (rc.w0 + lane)) & 1) ? 0xAAAAAAAAu : 0x55555555u) : 0u;
 
-		const uint32_t kk = dispatch_row<NREG>(a, w, lane, rc);  // 1 + deepest killer
+		const uint32_t kk = dispatch_row<NR2, NR3>(a, w, lane, rc);  // 1 + deepest killer
 		if (lane == 0 && kk) {
 			const uint32_t j = kk - 1;
 			const uint32_t killer = j < NREG ? a.reg_r[j < NREG ? j : 0] : __ldg(a.probes + j).x;
@@ -590,24 +601,34 @@ __global__ void k_classify(const uint64_t* __restrict__ pq, uint64_t n,
 	}
 }
 
-template <int NREG>
+template <int NR2, int NR3>
 void* sieve_fn()
 {
-	return reinterpret_cast<void*>(&k_sieve<NREG>);
+	return reinterpret_cast<void*>(&k_sieve<NR2, NR3>);
 }
 
-void* sieve_kernel_ptr(int nreg)
+// Instantiated: NR2 in 0..8 with NR3 = 0, and NR2 = 7 (every prime 11..31
+// killable -- all BASELINE sets) with NR3 in 1..kMaxReg3.
+void* sieve_kernel_ptr(int nr2, int nr3)
 {
-	switch (nreg) {
-	case 0: return sieve_fn<0>();
-	case 1: return sieve_fn<1>();
-	case 2: return sieve_fn<2>();
-	case 3: return sieve_fn<3>();
-	case 4: return sieve_fn<4>();
-	case 5: return sieve_fn<5>();
-	case 6: return sieve_fn<6>();
-	case 7: return sieve_fn<7>();
-	default: return sieve_fn<8>();
+	if (nr2 == 7 && nr3 > 0) {
+		switch (nr3) {
+		case 1: return sieve_fn<7, 1>();
+		case 2: return sieve_fn<7, 2>();
+		case 3: return sieve_fn<7, 3>();
+		default: return sieve_fn<7, 4>();
+		}
+	}
+	switch (nr2) {
+	case 0: return sieve_fn<0, 0>();
+	case 1: return sieve_fn<1, 0>();
+	case 2: return sieve_fn<2, 0>();
+	case 3: return sieve_fn<3, 0>();
+	case 4: return sieve_fn<4, 0>();
+	case 5: return sieve_fn<5, 0>();
+	case 6: return sieve_fn<6, 0>();
+	case 7: return sieve_fn<7, 0>();
+	default: return sieve_fn<8, 0>();
 	}
 }
 
@@ -618,11 +639,11 @@ __host__ __device__ size_t sieve_smem_bytes(uint32_t np)
 	return sizeof(uint32_t) * static_cast<size_t>(np) * kSieveWarps + sizeof(uint2) * kQueue * kSieveWarps;
 }
 
-int sieve_grid(int device, int nreg, size_t smem)
+int sieve_grid(int device, int nr2, int nr3, size_t smem)
 {
 	int sms = 0, per_sm = 0;
 	cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-	const void* fn = sieve_kernel_ptr(nreg);
+	const void* fn = sieve_kernel_ptr(nr2, nr3);
 	if (smem > 48 * 1024)
 		cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
 	cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kSieveThreads, smem);
@@ -640,7 +661,7 @@ cudaError_t launch_sieve(const SieveArgs& a, int grid, cudaStream_t s)
 {
 	const size_t smem = sieve_smem_bytes(a.np);
 	void* args[] = {const_cast<SieveArgs*>(&a)};
-	return cudaLaunchKernel(sieve_kernel_ptr(static_cast<int>(a.nreg)), dim3(grid),
+	return cudaLaunchKernel(sieve_kernel_ptr(static_cast<int>(a.nreg2), static_cast<int>(a.nreg3)), dim3(grid),
 	                        dim3(kSieveThreads), args, smem, s);
 }
 

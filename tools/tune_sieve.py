@@ -30,13 +30,16 @@ def main():
     libs = sys.argv[1].split(",")
     costs = sys.argv[2].split(",")
     wls = sys.argv[3] if len(sys.argv) > 3 else "C4,C5"
-    for lib, cost in itertools.product(libs, costs):
-        env = dict(os.environ, ROOT=ROOT, CUBOID_ROW_COST=cost)
+    regs = sys.argv[4].split(",") if len(sys.argv) > 4 else ["8"]
+    reg3 = sys.argv[5].split(",") if len(sys.argv) > 5 else ["4"]
+    for lib, cost, nreg, nr3 in itertools.product(libs, costs, regs, reg3):
+        env = dict(os.environ, ROOT=ROOT, CUBOID_ROW_COST=cost, CUBOID_MAX_REG_PROBES=nreg,
+                   CUBOID_REG3_PROBES=nr3)
         if lib != "default":
             env["CUBOID_GPU_LIB"] = os.path.join(ROOT, lib)
         r = subprocess.run([sys.executable, "-c", CHILD, wls], env=env, capture_output=True, text=True)
         res = json.loads(r.stdout.strip().splitlines()[-1]) if r.returncode == 0 else r.stderr[-500:]
-        print(f"lib={lib} row_cost={cost} {res}", flush=True)
+        print(f"lib={lib} row_cost={cost} reg2={nreg} reg3={nr3} {res}", flush=True)
 
 
 if __name__ == "__main__":
