@@ -6,9 +6,9 @@
 
 One "step" = one pass of the hot path over the workload: the (p,q) pair sieve
 of BASELINE.json's config against resident residue tables, with the
-cross-rank reduction of its results (NCCL all-reduce of pair/survivor counts
-and the first-killer histogram, max-reduce of block r_max, gather of survivor
-lists). Rows are split block-cyclically over ranks (p/100 blocks), so the
+cross-rank reduction of its results (ONE NCCL all-reduce(SUM) of a packed
+buffer: pair/survivor counts, the first-killer histogram, block r_max -- each
+block has one owner, the others hold 0 -- and per-rank survivor slices). Rows are split block-cyclically over ranks (p/100 blocks), so the
 total work is fixed as N grows ("strong" scaling).
 
 `value` = pairs sieved per second over the timed steps, inputs resident in HBM,
@@ -321,32 +321,38 @@ def run_ours(args, wl, primes):
     n = len(primes)
     G, g = world, rank
     nblocks = wl["p_hi"] // 100 - wl["p_lo"] // 100 + 1
-    acc = torch.zeros(2 + n, dtype=torch.int64, device=cuda)  # [pairs, survivors, hist...]
-    brm = torch.zeros(nblocks, dtype=torch.int32, device=cuda)
-    surv = torch.zeros(GATHER_CAP, dtype=torch.int64, device=cuda)
-    gath = torch.zeros(GATHER_CAP * world, dtype=torch.int64, device=cuda)
+    # One int64 exchange buffer, reduced by ONE all-reduce(SUM) per step:
+    #   [pairs, survivors, hist(n) | block r_max (nblocks) | survivors (world x cap)]
+    # Block r_max needs no MAX: every p/100 block is owned by exactly one rank
+    # and the others hold 0 (k_init_blocks). Each rank writes its survivors
+    # into its own slice of a zeroed region, so the SUM is the gather.
+    n_acc, n_surv = 2 + n, world * GATHER_CAP
+    buf = torch.zeros(n_acc + nblocks + n_surv, dtype=torch.int64, device=cuda)
+    acc = buf[:n_acc]
+    brm_sum = buf[n_acc:n_acc + nblocks]
+    surv_all = buf[n_acc + nblocks:]
+    brm = torch.zeros(nblocks, dtype=torch.int32, device=cuda)  # the kernel writes u32 r_max
+    surv_mine = surv_all[g * GATHER_CAP:(g + 1) * GATHER_CAP]
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=cuda)  # > 126 MB L2
 
     def launch():
+        if world > 1:
+            surv_all.zero_()
         N.check(L.cgpu_sieve_launch_dev(
             dev._ctx, wl["p_lo"], 0, wl["p_hi"], N.TRIANGLE, G, g,
             C.c_void_p(acc.data_ptr()), C.c_void_p(acc.data_ptr() + 16), C.c_void_p(brm.data_ptr()),
-            nblocks, C.c_void_p(surv.data_ptr()), GATHER_CAP))
+            nblocks, C.c_void_p(surv_mine.data_ptr()), GATHER_CAP))
 
     def exchange():
-        if world > 1 and not gloo:
-            dist.all_reduce(acc, op=dist.ReduceOp.SUM)
-            dist.all_reduce(brm, op=dist.ReduceOp.MAX)
-            dist.all_gather_into_tensor(gath, surv)
-        elif world > 1:  # gloo: stage through host memory
-            a, b, sv = acc.cpu(), brm.cpu(), surv.cpu()
-            gv = torch.zeros(GATHER_CAP * world, dtype=torch.int64)
-            dist.all_reduce(a, op=dist.ReduceOp.SUM)
-            dist.all_reduce(b, op=dist.ReduceOp.MAX)
-            dist.all_gather_into_tensor(gv, sv)
-            acc.copy_(a)
-            brm.copy_(b)
-            gath.copy_(gv)
+        if world == 1:
+            return
+        brm_sum.copy_(brm)
+        if gloo:  # stage through host memory
+            h = buf.cpu()
+            dist.all_reduce(h, op=dist.ReduceOp.SUM)
+            buf.copy_(h)
+        else:
+            dist.all_reduce(buf, op=dist.ReduceOp.SUM)
 
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
@@ -372,25 +378,24 @@ def run_ours(args, wl, primes):
     # results of the last step (already reduced across ranks)
     res = acc.cpu().numpy()
     pairs, survivors, hist = int(res[0]), int(res[1]), res[2:]
-    parity_ok = (pairs == wl["pairs"] and int(hist.sum()) + survivors == pairs)
+    blocks_ok = bool((brm_sum if world > 1 else brm).min().item() >= 1)  # every block reduced once
+    parity_ok = (pairs == wl["pairs"] and int(hist.sum()) + survivors == pairs and blocks_ok)
     local_pairs = pairs if world == 1 else None
 
     # ---- e2e: host tables in, host results out, through the C ABI -------------------------
     pinned = torch.empty(len(tables), dtype=torch.uint8, pin_memory=True)
     pinned.numpy()[:] = np.frombuffer(tables, np.uint8)
     pr = np.ascontiguousarray(primes, dtype=np.uint32)
-    h_acc = torch.empty(2 + n, dtype=torch.int64, pin_memory=True)
-    h_brm = torch.empty(nblocks, dtype=torch.int32, pin_memory=True)
-    h_surv = torch.empty(GATHER_CAP * world, dtype=torch.int64, pin_memory=True)
+    h_buf = torch.empty(buf.numel(), dtype=torch.int64, pin_memory=True)
 
     def e2e_step():
         N.check(L.cgpu_tables_load(dev._ctx, pr.ctypes.data_as(C.c_void_p), n,
                                    C.c_void_p(pinned.data_ptr()), len(tables)))
         launch()
         exchange()
-        h_acc.copy_(acc, non_blocking=True)
-        h_brm.copy_(brm, non_blocking=True)
-        h_surv.copy_(gath if world > 1 else surv, non_blocking=True)
+        if world == 1:
+            brm_sum.copy_(brm)
+        h_buf.copy_(buf, non_blocking=True)
         stream.synchronize()
 
     for _ in range(args.warmup):
@@ -404,14 +409,14 @@ def run_ours(args, wl, primes):
     barrier()
     e2e_total = allreduce_max(float(np.sum(e2e_s)))
     clk.__exit__()
-    parity_ok = parity_ok and int(h_acc[0]) == wl["pairs"]
+    parity_ok = parity_ok and int(h_buf[0]) == wl["pairs"]
 
     # ---- roofline of the dominant kernel (k_sieve), rank-local ------------------------------
     if world > 1:  # this rank's own pairs for the per-launch figure
         N.check(L.cgpu_sieve_launch_dev(
             dev._ctx, wl["p_lo"], 0, wl["p_hi"], N.TRIANGLE, G, g,
             C.c_void_p(acc.data_ptr()), C.c_void_p(acc.data_ptr() + 16), C.c_void_p(brm.data_ptr()),
-            nblocks, C.c_void_p(surv.data_ptr()), GATHER_CAP))
+            nblocks, C.c_void_p(surv_mine.data_ptr()), GATHER_CAP))
         local_pairs = int(acc[0].item())
     opp, d_eff, omega_bar = ops_per_pair(primes, killable, hist, survivors, pairs,
                                          wl["p_lo"], wl["p_hi"])
@@ -444,12 +449,12 @@ def run_ours(args, wl, primes):
             "config": {"workload": wl["desc"], "primes": n, "p_range": [wl["p_lo"], wl["p_hi"]],
                        "mode": "TRIANGLE", "pairs_per_step": pairs,
                        "l2": "flushed between steps (512 MiB write)",
-                       "parallelism": f"dp{world}: p/100 blocks block-cyclic over ranks, "
-                                      "NCCL all-reduce of counts/histogram/r_max + survivor all-gather"},
+                       "parallelism": f"dp{world}: p/100 blocks block-cyclic over ranks, one NCCL "
+                                      "all-reduce(SUM) of counts/histogram/block r_max/survivor slices"},
             "parity": "ok" if parity_ok else "MISMATCH",
             "e2e": {"value": pairs * args.steps / e2e_total, "unit": "pairs/s",
                     "h2d_bytes_per_step": len(tables) + 4 * n,
-                    "d2h_bytes_per_step": 8 * (2 + n) + 4 * nblocks + 8 * GATHER_CAP * world,
+                    "d2h_bytes_per_step": 8 * buf.numel(),
                     "ms_per_step": 1e3 * e2e_total / args.steps,
                     "path": "cgpu_tables_load(host tables) + cgpu_sieve_launch_dev + reduce + D2H"},
             "gpu_launches": launches,

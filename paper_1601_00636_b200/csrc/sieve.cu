@@ -35,6 +35,7 @@ namespace cgpu {
 namespace {
 
 constexpr uint32_t kFull = 0xffffffffu;
+constexpr uint32_t kDeepPrefetch = 8;  // deep probes whose rows are prefetched per row
 constexpr uint32_t kStepQ = 32 * 32;  // q advance per warp iteration per lane
 
 // least q >= 1 with 9 q^3 >= p (region.hpp:25-39) / q_bounds (region.hpp:49-63)
@@ -531,6 +532,15 @@ __global__ void __launch_bounds__(kSieveThreads, kSieveMinBlocks) k_sieve(const 
 		// q0 parity is fixed per lane (q advances by 32 per window): even p
 		// excludes the even q of every window
 		rc.even = even ? (((rc.qlo + 32 * (rc.w0 + lane)) & 1) ? 0xAAAAAAAAu : 0x55555555u) : 0u;
+#ifndef CGPU_NO_DEEP_PREFETCH
+		// pull the rows of the first deep probes into L1: every drain of this
+		// row walks them first (lanes 2k, 2k+1 take the two lines of probe k)
+		if (NREG + lane / 2 < a.np && lane < 2 * kDeepPrefetch) {
+			const uint4 d = __ldg(a.probes + NREG + lane / 2);
+			const uint32_t* row = a.ext + d.z + mod_full(rc.p, d.x, d.y) * d.w + (lane & 1) * 32;
+			if ((lane & 1) == 0 || d.w > 32) asm volatile("prefetch.global.L1 [%0];" ::"l"(row));
+		}
+#endif
 
 		const uint32_t kk = dispatch_row<NR2, NR3>(a, w, lane, rc);  // 1 + deepest killer
 		if (lane == 0 && kk) {

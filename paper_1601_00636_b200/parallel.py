@@ -7,9 +7,12 @@ balances the linearly growing row lengths and keeps every block on one rank.
 Each rank sieves its blocks into device buffers (cgpu_sieve_launch_dev) and
 the ranks then combine exactly as ScanStats::merge does (engine.hpp:121-134):
 
-    sum  : pairs_tested, survivors, first-killer histogram   (all_reduce SUM)
-    max  : block r_max (0 marks blocks a rank does not own)    (all_reduce MAX)
-    cat  : survivor lists, then sorted to canonical (p, q)     (all_gather)
+    sum  : pairs_tested, survivors, first-killer histogram
+    max  : block r_max (0 marks blocks a rank does not own)
+    cat  : survivor lists, then sorted to canonical (p, q)
+
+reduce_packed does all three in one all_reduce(SUM) (one owner per block, one
+slice per rank); reduce_results + gather_survivors is the plain form.
 
 The same reduction code runs on CPU tensors over gloo (tests) and on CUDA
 tensors over NCCL (the product path and bench.py).
@@ -44,6 +47,37 @@ def reduce_results(acc, brm, group=None):
     dist.all_reduce(acc, op=dist.ReduceOp.SUM, group=group)
     dist.all_reduce(brm, op=dist.ReduceOp.MAX, group=group)
     return acc, brm
+
+
+def reduce_packed(acc, brm, keys, count: int, cap: int, group=None):
+    """The whole cross-rank merge in ONE all-reduce(SUM) of a packed int64
+    buffer [acc | block r_max | per-rank count | per-rank survivor slices]:
+    block r_max needs no MAX because every p/100 block has exactly one owner
+    (the others hold 0), and each rank's survivors land in its own zeroed
+    slice, so the sum is the gather. Falls back to gather_survivors when some
+    rank has more than `cap` survivors. Returns (acc, brm, sorted (p, q))."""
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    na, nb = acc.numel(), brm.numel()
+    buf = torch.zeros(na + nb + world + world * cap, dtype=torch.int64, device=acc.device)
+    buf[:na] = acc
+    buf[na:na + nb] = brm.to(torch.int64)
+    buf[na + nb + rank] = count
+    k = min(count, cap)
+    base = na + nb + world + rank * cap
+    buf[base:base + k] = keys[:k]
+    dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=group)
+    acc.copy_(buf[:na])
+    brm.copy_(buf[na:na + nb].to(brm.dtype))
+    counts = buf[na + nb:na + nb + world].cpu().numpy()
+    if counts.max() > cap:
+        return acc, brm, gather_survivors(keys, count, group)
+    surv = buf[na + nb + world:].view(world, cap).cpu().numpy()
+    allk = np.concatenate([surv[r][:counts[r]] for r in range(world)]).astype(np.uint64)
+    allk.sort()
+    return acc, brm, np.stack([allk >> np.uint64(32), allk & np.uint64(0xFFFFFFFF)], 1)
 
 
 def gather_survivors(keys, count: int, group=None):
@@ -108,8 +142,8 @@ class ShardedSieve:
             raise N.CudaSieveError(N.ERR_CAPACITY, f"{local_surv} survivors exceed {self.surv_cap}")
         keys = self.surv
         if dist.is_initialized() and dist.get_world_size() > 1:
-            reduce_results(self.acc, self.brm[:max(self.nb, 1)])
-            pairs = gather_survivors(keys, local_surv)
+            _, _, pairs = reduce_packed(self.acc, self.brm[:max(self.nb, 1)], keys, local_surv,
+                                        cap=4096)
         else:
             k = np.sort(keys[:local_surv].cpu().numpy().astype(np.uint64))
             pairs = np.stack([k >> np.uint64(32), k & np.uint64(0xFFFFFFFF)], 1)

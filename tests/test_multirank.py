@@ -81,8 +81,13 @@ def _worker(rank, world, port_, case, out):
     acc_t, brm_t = torch.from_numpy(acc), torch.from_numpy(brm)
     keys_t = torch.zeros(max(len(keys), 1), dtype=torch.int64)
     keys_t[:len(keys)] = torch.from_numpy(keys)
+    acc2, brm2 = acc_t.clone(), brm_t.clone()
     parallel.reduce_results(acc_t, brm_t)
     surv = parallel.gather_survivors(keys_t, len(keys))
+    # the single-collective form, with a cap small enough to hit the fallback too
+    _, _, surv2 = parallel.reduce_packed(acc2, brm2, keys_t, len(keys), cap=64)
+    assert acc2.tolist() == acc_t.tolist() and brm2.tolist() == brm_t.tolist()
+    assert surv2.tolist() == surv.tolist()
     out[rank] = (acc_t.numpy().tolist(), brm_t.numpy().tolist(), surv.tolist())
     dist.destroy_process_group()
 
