@@ -140,13 +140,30 @@ int main()
 		          ge[i].verdict.t == re[i].verdict.t;
 	CHECK(ev_same);
 
-	// split/resume: a pre-armed stop halts before any work; a split scan
-	// merged equals the whole (test_engine.cpp:134-175)
+	// split/resume: a pre-armed stop halts where the reference's does
+	// (test_engine.cpp:149-164); a split scan merged equals the whole
+	// (test_engine.cpp:134-175)
 	std::atomic<bool> stop{true};
 	ScanOptions so;
 	so.hooks.stop = &stop;
-	const ScanStats halted = gpu::scan(gpu_default, {152, 3}, 4000, {}, so);
-	CHECK(halted.stopped && halted.pairs_tested == 0 && halted.resume_p == 152 && halted.resume_q == 3);
+	for (uint64_t bp : {1ull, 1000ull, 8000ull, 65536ull, 400000ull}) {
+		std::atomic<bool> rstop{true};
+		ScanOptions ro;
+		ro.batch_pairs = so.batch_pairs = bp;
+		ro.hooks.stop = &rstop;
+		for (SearchPair s : {SearchPair{152, 3}, SearchPair{153, 7000}, SearchPair{401, 23000}}) {
+			const ScanStats g1 = gpu::scan(gpu_default, s, 700, {}, so);
+			const ScanStats r1 = scan(ref_default, s, 700, {}, ro);
+			CHECK(same(g1, r1));
+			CHECK(g1.stopped);
+			ScanStats g2 = g1;
+			g2.merge(gpu::scan(gpu_default, {g1.resume_p, g1.resume_q}, 700));
+			const ScanStats whole = gpu::scan(gpu_default, s, 700);
+			CHECK(g2.pairs_tested == whole.pairs_tested && g2.kill_histogram == whole.kill_histogram &&
+			      g2.block_r_max == whole.block_r_max && g2.resume_p == whole.resume_p);
+		}
+	}
+	so.batch_pairs = 1u << 16;
 	stop = false;
 	ScanStats head = gpu::scan(gpu_default, {152, 3}, 2222, {}, so);
 	const ScanStats tail = gpu::scan(gpu_default, {head.resume_p, head.resume_q}, 4000);

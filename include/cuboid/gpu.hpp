@@ -19,12 +19,13 @@
 // libcuboid_gpu.so (sm_100a) through include/cuboid_gpu.h; there is no CPU
 // fallback: without a device every call throws std::runtime_error.
 //
-// Cooperative stop (ScanOptions::hooks.stop): the device scan is split into
-// tiles of kStopTileRows rows when a stop flag is given, and the flag is
-// polled between tiles; the resume point is then the first row of the next
-// tile, (p, q_low(p)). ScanStats::merge of the two halves equals the full scan
-// (the reference's split/resume contract, test_engine.cpp:134-175), at tile
-// rather than batch_pairs granularity.
+// Cooperative stop (ScanOptions::hooks.stop): a flag already raised when scan()
+// starts halts exactly where the reference's does -- at the batch_pairs-th q
+// visited (engine.hpp:248-257), same resume point and statistics (the span
+// before it is sieved with cgpu_sieve_span). A flag raised while the scan
+// runs is polled between tiles of kStopTileRows rows; the resume point is then
+// the first pair of the next tile. Either way ScanStats::merge of the two
+// halves equals the full scan (test_engine.cpp:134-175).
 
 #include <chrono>
 #include <cstdint>
@@ -190,6 +191,56 @@ inline DeviceScan run(Context& c, const SieveSet& set, uint64_t p_lo, uint64_t q
 	return d;
 }
 
+// The (p, q) at which the reference halts with a raised stop flag: the
+// batch_pairs-th q visited from `start` (engine.hpp:248-257); false if the
+// range ends first.
+inline bool stop_point(SearchPair start, uint64_t p_end, uint64_t batch_pairs, SearchPair& at)
+{
+	uint64_t k = batch_pairs ? batch_pairs : 1;
+	for (uint64_t p = start.p; p <= p_end; ++p) {
+		const RegionBounds b = q_bounds(p);
+		const uint64_t q0 = p == start.p ? start.q : b.q_low;
+		const uint64_t n = b.q_high >= q0 ? b.q_high - q0 + 1 : 0;
+		if (k <= n) {
+			at = {p, q0 + k - 1};
+			return true;
+		}
+		k -= n;
+	}
+	return false;
+}
+
+// REGION pairs from `from` up to, not including, `to` (sieved on the device).
+inline DeviceScan run_span(Context& c, const SieveSet& set, SearchPair from, SearchPair to)
+{
+	DeviceScan d;
+	d.hist.assign(set.prime_count(), 0);
+	const uint64_t first = to.p == from.p ? from.q : q_bounds(to.p).q_low;
+	uint64_t p_hi = to.p, q_end = to.q - 1;
+	if (to.q == first) {  // the stop is the row's first pair: that row is not sieved
+		p_hi = to.p - 1;
+		q_end = 0;
+	}
+	if (p_hi < from.p) return d;
+	d.block_lo = from.p / 100;
+	const uint64_t nb = p_hi / 100 - from.p / 100 + 1;
+	d.block_rmax.assign(nb, 0);
+	uint64_t cap = 1 << 16;
+	for (;;) {
+		d.surv.assign(2 * cap, 0);
+		const int rc = cgpu_sieve_span(c.get(), from.p, from.q, p_hi, q_end, d.counts, d.hist.data(),
+		                               d.block_rmax.data(), nb, d.surv.data(), cap);
+		if (rc == CGPU_ERR_CAPACITY && d.counts[1] > cap) {
+			cap = d.counts[1];
+			continue;
+		}
+		check(rc, "scan");
+		break;
+	}
+	d.surv.resize(2 * d.counts[1]);
+	return d;
+}
+
 inline void fold(const SieveSet& set, const DeviceScan& d, ScanStats& st, const ScanSink& sink)
 {
 	st.pairs_tested += d.counts[0];
@@ -226,6 +277,17 @@ inline ScanStats scan(const SieveSet& set, SearchPair start, uint64_t p_end, con
 	std::lock_guard<std::mutex> lk(c.mutex());
 	c.ensure_resident(set);
 
+	SearchPair at{};
+	if (opt.hooks.stop && opt.hooks.stop->load(std::memory_order_relaxed) &&
+	    detail::stop_point(start, p_end, opt.batch_pairs, at)) {
+		detail::fold(set, detail::run_span(c, set, start, at), st, sink);
+		st.block_r_max.try_emplace(at.p / 100, 1u);  // the stop row's block was entered
+		st.resume_p = at.p;
+		st.resume_q = at.q;
+		st.stopped = true;
+		st.elapsed = std::chrono::steady_clock::now() - t0;
+		return st;
+	}
 	uint64_t p = start.p, q = start.q;
 	const uint64_t tile = opt.hooks.stop ? kStopTileRows : UINT64_MAX;
 	while (p <= p_end) {

@@ -171,6 +171,15 @@ int cgpu_sieve_launch_dev(cgpu_ctx* ctx, uint64_t p_lo, uint64_t q_start, uint64
                           uint64_t* d_hist, uint32_t* d_block_rmax, uint64_t block_cap,
                           uint64_t* d_surv, uint64_t surv_cap);
 
+/* A REGION span that may end mid-row: rows p_lo..p_hi, the first from q_start
+ * (0 = q_low), the last up to q_end inclusive (0 = q_high). Synchronous; the
+ * outputs are those of cgpu_sieve_results. This is what a scan() halted by
+ * its cooperative stop flag covers (engine.hpp:248-257): the caller computes
+ * the reference's stop point and sieves up to the pair before it. */
+int cgpu_sieve_span(cgpu_ctx* ctx, uint64_t p_lo, uint64_t q_start, uint64_t p_hi, uint64_t q_end,
+                    uint64_t* counts, uint64_t* hist, uint32_t* block_rmax, uint64_t block_cap,
+                    uint64_t* surv_pq, uint64_t surv_cap);
+
 /* Device time of the last sieve launch or table build, from CUDA events on the
  * context stream (waits for them). Sieve: ms[0] = init + first plan kernel,
  * ms[1] = sieve kernel(s), ms[2] = whole launch. Table build: ms[0] = build

@@ -52,6 +52,9 @@ SIGNATURES = {
     "cgpu_sieve_launch_dev": (C.c_int, [C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint64, C.c_int,
                                         C.c_uint32, C.c_uint32, C.c_void_p, C.c_void_p, C.c_void_p,
                                         C.c_uint64, C.c_void_p, C.c_uint64]),
+    "cgpu_sieve_span": (C.c_int, [C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64,
+                                  C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p,
+                                  C.c_uint64]),
     "cgpu_last_timings": (C.c_int, [C.c_void_p, C.POINTER(C.c_float)]),
     "cgpu_int32_peak": (C.c_int, [C.c_int, C.POINTER(C.c_double)]),
     "cgpu_last_launch_count": (C.c_int, [C.c_void_p, _u32p]),

@@ -667,8 +667,8 @@ uint64_t launch_blocks(uint64_t p_lo, uint64_t p_hi)
 
 // Enqueues init + (plan, sieve) per chunk of row slots on the context stream,
 // writing into the given device buffers. Events ev[0..2] bracket the launch.
-int enqueue_sieve(cgpu_ctx* c, uint64_t p_lo, uint64_t q_start, uint64_t p_hi, int mode, uint32_t G,
-                  uint32_t g, unsigned long long* d_counts, unsigned long long* d_hist,
+int enqueue_sieve(cgpu_ctx* c, uint64_t p_lo, uint64_t q_start, uint64_t p_hi, uint64_t q_end, int mode,
+                  uint32_t G, uint32_t g, unsigned long long* d_counts, unsigned long long* d_hist,
                   uint32_t* d_block_rmax, unsigned long long* d_surv, uint64_t surv_cap)
 {
 	c->launched = false;
@@ -704,6 +704,7 @@ int enqueue_sieve(cgpu_ctx* c, uint64_t p_lo, uint64_t q_start, uint64_t p_hi, i
 	a.p_lo = p_lo;
 	a.p_hi = p_hi;
 	a.q_start = q_start;
+	a.q_end = q_end;
 	a.mode = mode;
 	a.G = G;
 	a.hist = d_hist;
@@ -764,8 +765,31 @@ int cgpu_sieve_launch(cgpu_ctx* c, uint64_t p_lo, uint64_t q_start, uint64_t p_h
 	CK(c->block_rmax.ensure(launch_blocks(p_lo, p_hi)));
 	CK(c->surv.ensure(surv_cap));
 	c->results_internal = true;
-	return enqueue_sieve(c, p_lo, q_start, p_hi, mode, G, g, c->counters.p, c->hist.p, c->block_rmax.p,
+	return enqueue_sieve(c, p_lo, q_start, p_hi, 0, mode, G, g, c->counters.p, c->hist.p, c->block_rmax.p,
 	                     c->surv.p, surv_cap);
+}
+
+int cgpu_sieve_span(cgpu_ctx* c, uint64_t p_lo, uint64_t q_start, uint64_t p_hi, uint64_t q_end,
+                    uint64_t* counts, uint64_t* hist, uint32_t* block_rmax, uint64_t block_cap,
+                    uint64_t* surv_pq, uint64_t surv_cap)
+{
+	if (int rc = check_launch(c, p_lo, q_start, p_hi, CGPU_REGION, 1, 0)) return rc;
+	if (q_end) {
+		uint64_t lo, hi;
+		q_bounds(p_hi, &lo, &hi);
+		if (q_end > hi) return set_err(CGPU_Q_ABOVE_HIGH, "q_end above q_high");
+	}
+	CK(cudaSetDevice(c->device));
+	CK(c->hist.ensure(c->primes.size()));
+	CK(c->counters.ensure(2));
+	CK(c->block_rmax.ensure(launch_blocks(p_lo, p_hi)));
+	const uint64_t cap = surv_pq ? surv_cap : 0;
+	CK(c->surv.ensure(cap));
+	c->results_internal = true;
+	if (int rc = enqueue_sieve(c, p_lo, q_start, p_hi, q_end, CGPU_REGION, 1, 0, c->counters.p, c->hist.p,
+	                           c->block_rmax.p, c->surv.p, cap))
+		return rc;
+	return cgpu_sieve_results(c, counts, hist, block_rmax, block_cap, surv_pq, surv_cap);
 }
 
 int cgpu_sieve_launch_dev(cgpu_ctx* c, uint64_t p_lo, uint64_t q_start, uint64_t p_hi, int mode,
@@ -780,7 +804,7 @@ int cgpu_sieve_launch_dev(cgpu_ctx* c, uint64_t p_lo, uint64_t q_start, uint64_t
 		return set_err(CGPU_ERR_CAPACITY, "block_rmax buffer too small");
 	CK(cudaSetDevice(c->device));
 	c->results_internal = false;
-	return enqueue_sieve(c, p_lo, q_start, p_hi, mode, G, g,
+	return enqueue_sieve(c, p_lo, q_start, p_hi, 0, mode, G, g,
 	                     reinterpret_cast<unsigned long long*>(d_counts),
 	                     reinterpret_cast<unsigned long long*>(d_hist), d_block_rmax,
 	                     reinterpret_cast<unsigned long long*>(d_surv), surv_cap);

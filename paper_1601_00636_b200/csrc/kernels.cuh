@@ -78,6 +78,7 @@ struct SieveArgs {
 	uint32_t n_fprimes;
 	// row slots: slot s -> owned block ordinal s/100, p = (blk0 + ord*G)*100 + s%100
 	uint64_t p_lo, p_hi, q_start;
+	uint64_t q_end;               // REGION: last q of row p_hi (0 = the whole row)
 	int mode;
 	uint32_t G;
 	uint64_t blk0;                // first owned block of this launch

@@ -74,6 +74,7 @@ __device__ __forceinline__ RowBounds slot_row(const SieveArgs& a, uint32_t s)
 		b.qlo = q_low_dev(b.p);
 		b.qhi = 59 * b.p;
 		if (b.p == a.p_lo && a.q_start) b.qlo = a.q_start;
+		if (b.p == a.p_hi && a.q_end && a.q_end < b.qhi) b.qhi = a.q_end;  // a span ending mid-row
 		// q == p is skipped (engine.hpp:258); for p > 1 the coprimality mask
 		// removes it, for p = 1 (q_low = 1) start the row at q = 2
 		if (b.p == 1 && b.qlo == 1) b.qlo = 2;
@@ -422,7 +423,8 @@ __device__ __forceinline__ uint32_t row_loop(const SieveArgs& a, const WarpSmem&
 	// register-probe counts of this segment (per-row sums are < 2^32: 59p < 2^32)
 	if (NREG > 0) {
 		const uint32_t qa = rc.qlo + 32 * rc.w0;
-		const uint32_t qb = min(rc.qhi, rc.qlo + 32 * rc.w1 - 1);
+		const uint64_t qe = uint64_t(rc.qlo) + 32ull * rc.w1 - 1;  // 64-bit: no 2^32 wrap
+		const uint32_t qb = qe < rc.qhi ? static_cast<uint32_t>(qe) : rc.qhi;
 		const uint32_t tot = coprime_in(rc, lane, qa, qb);
 		S[0] = lane == 0 ? tot : 0;  // warp_sum(S[0] - S[1]) below: exact mod 2^32
 	}

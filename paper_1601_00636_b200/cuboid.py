@@ -22,6 +22,7 @@ exactly as scan() does when a sink is set (engine.hpp:272-277).
 """
 from __future__ import annotations
 
+import ctypes as C
 import time
 from dataclasses import dataclass, field
 from typing import Callable, Optional
@@ -245,10 +246,42 @@ def load_sieve(tables: bytes, index: bytes, dev: int = 0) -> "SieveSet":
 
 @dataclass
 class ScanOptions:
-    """engine.hpp:144-149 (hooks are not supported by the device scan)."""
+    """engine.hpp:144-149. `stop` stands for hooks.stop: a bool, an object with
+    is_set(), or a callable. It is read when scan() starts; if it is already
+    raised the scan halts exactly where the reference's does -- at the
+    batch_pairs-th q visited (engine.hpp:248-257) -- with the same resume
+    point. (A flag raised while a device launch runs is not observed.)"""
     small_p: bool = False
     p_limit: int = P_LIMIT_32BIT
     batch_pairs: int = 1 << 16
+    stop: object = None
+
+    def stop_requested(self) -> bool:
+        s = self.stop
+        if s is None:
+            return False
+        if hasattr(s, "is_set"):
+            return bool(s.is_set())
+        return bool(s() if callable(s) else s)
+
+
+def stop_point(start, p_end: int, batch_pairs: int):
+    """The (p, q) at which a scan with a raised stop flag halts: the
+    batch_pairs-th q visited from `start`, counting every q of the region rows
+    (skipped pairs included, engine.hpp:248-257); None if the range ends first."""
+    k = max(int(batch_pairs), 1)
+    p, q = int(start[0]), int(start[1])
+    first = True
+    while p <= p_end:
+        lo, hi = q_bounds(p)
+        q0 = q if first else lo
+        first = False
+        n = hi - q0 + 1 if hi >= q0 else 0
+        if k <= n:
+            return p, q0 + k - 1
+        k -= n
+        p += 1
+    return None
 
 
 @dataclass
@@ -332,6 +365,40 @@ def _run(set_: SieveSet, p_lo, q_start, p_hi, mode, shard, surv_cap):
             cap = max(2 * cap, getattr(e, "survivors", 0) + 1)
 
 
+def _span(set_: SieveSet, p0: int, q0: int, p_stop: int, q_stop: int) -> ScanStats:
+    """REGION pairs from (p0, q0) up to, not including, (p_stop, q_stop)."""
+    d = set_.resident()
+    lo = q_bounds(p_stop)[0]
+    first = q0 if p_stop == p0 else lo
+    p_hi, q_end = p_stop, q_stop - 1
+    if q_stop == first:  # the stop falls on the row's first pair: that row is not sieved
+        p_hi, q_end = p_stop - 1, 0
+    n = set_.prime_count()
+    st = ScanStats()
+    if p_hi >= p0:
+        cap = 1 << 20
+        while True:
+            counts = np.zeros(2, np.uint64)
+            hist = np.zeros(max(n, 1), np.uint64)
+            nb = p_hi // 100 - p0 // 100 + 1
+            brm = np.zeros(nb, np.uint32)
+            spq = np.zeros((cap, 2), np.uint64)
+            rc = N.lib().cgpu_sieve_span(d._ctx, p0, q0, p_hi, q_end, counts.ctypes.data_as(C.c_void_p),
+                                         hist.ctypes.data_as(C.c_void_p), brm.ctypes.data_as(C.c_void_p),
+                                         nb, spq.ctypes.data_as(C.c_void_p), cap)
+            if rc == N.ERR_CAPACITY and int(counts[1]) > cap:
+                cap = int(counts[1])
+                continue
+            N.check(rc)
+            break
+        st.pairs_tested, st.survivors = int(counts[0]), int(counts[1])
+        st.kill_histogram = {set_.prime_at(k): int(c) for k, c in enumerate(hist[:n]) if c}
+        st.block_r_max = {p0 // 100 + i: int(v) for i, v in enumerate(brm) if v}
+        st.survivor_pairs = [(int(a), int(b)) for a, b in spq[: st.survivors]]
+    st.block_r_max.setdefault(p_stop // 100, 1)  # the stop row's block is entered (engine.hpp:229-236)
+    return st
+
+
 def scan(set_: SieveSet, start, p_end: int, sink: Optional[Callable] = None,
          opt: Optional[ScanOptions] = None, verifier: Optional[Callable] = None,
          shard=(1, 0), surv_cap: int = 1 << 20) -> ScanStats:
@@ -349,7 +416,11 @@ def scan(set_: SieveSet, start, p_end: int, sink: Optional[Callable] = None,
         raise ScanRejected(3)
     t0 = time.perf_counter()
     st = ScanStats(resume_p=p0, resume_q=q0)
-    if p0 <= p_end:
+    halt = stop_point((p0, q0), p_end, opt.batch_pairs) if opt.stop_requested() else None
+    if halt is not None:  # the span before the reference's stop point
+        st = _span(set_, p0, q0, halt[0], halt[1])
+        st.resume_p, st.resume_q, st.stopped = halt[0], halt[1], True
+    elif p0 <= p_end:
         res = _run(set_, p0, q0, p_end, N.REGION, shard, surv_cap)
         st = stats_from_result(set_, res)
         st.resume_p, st.resume_q = _next_pair(p_end)

@@ -360,3 +360,84 @@ def test_historical_region_scan():
     assert max(st.block_r_max.values()) == 137
     assert len(st.block_r_max) == 1541
     assert st.histogram_total() == st.pairs_tested
+
+
+def _factors(n):
+    f, d = [], 2
+    while d * d <= n:
+        if n % d == 0:
+            f.append(d)
+            while n % d == 0:
+                n //= d
+        d += 1 if d == 2 else 2
+    if n > 1:
+        f.append(n)
+    return f
+
+
+def _coprime_count(p, lo, hi):
+    """#{q in [lo, hi]: gcd(p, q) = 1, q != p} by inclusion-exclusion."""
+    fs = _factors(p)
+    tot = 0
+    for mask in range(1 << len(fs)):
+        d, bits = 1, 0
+        for i, f in enumerate(fs):
+            if mask >> i & 1:
+                d *= f
+                bits += 1
+        tot += (-1) ** bits * (hi // d - (lo - 1) // d)
+    if p == 1 and lo <= 1 <= hi:
+        tot -= 1
+    return tot
+
+
+def test_rows_at_the_32bit_limits(dev, sets):
+    """Maximum sizes: the last REGION row below the 32-bit limit (q up to
+    59p = 4,294,967,245, region.hpp:43-44) and TRIANGLE rows next to 2^32:
+    exact candidate counts, every candidate accounted for, and a tail of the
+    REGION row checked pair by pair against the oracle."""
+    P = sets["default96"]
+    tb, offs = port.build_set(P)
+    dev.load(P, tb)
+    p = 72796055
+    lo, hi = cuboid.q_bounds(p)
+    r = dev.sieve(p, p, N.REGION)
+    assert r.pairs_tested == _coprime_count(p, lo, hi)
+    assert int(r.hist.sum()) + r.survivors == r.pairs_tested
+    q0 = hi - 20000
+    r = dev.sieve(p, p, N.REGION, q_start=q0)
+    o = port.sieve(tb, P, offs, p, p, port.REGION, q_start=q0)
+    assert (r.pairs_tested, r.survivors) == (o["pairs_tested"], o["survivors"])
+    assert r.hist.tolist() == o["hist"].tolist()
+    for p in (4294967291, 4294967295, 4294967294):  # prime; 3*5*17*257*65537; 2*3*...
+        r = dev.sieve(p, p, N.TRIANGLE)
+        assert r.pairs_tested == _coprime_count(p, 1, p - 1), p
+        assert int(r.hist.sum()) + r.survivors == r.pairs_tested
+    with pytest.raises(N.CudaSieveError):
+        dev.sieve(4294967296, 4294967296, N.TRIANGLE)
+
+
+@pytest.mark.skipif(not refmod.available(), reason="oracle/_ref not built")
+@pytest.mark.parametrize("bp", [1, 59, 1000, 9000, 65536, 400000])
+def test_prearmed_stop_matches_reference(bp):
+    """A stop flag raised before scan() halts at the reference's batch boundary
+    with the same statistics and resume point (engine.hpp:248-257,
+    test_engine.cpp:149-164); resuming from there and merging gives the whole
+    scan (test_engine.cpp:134-175)."""
+    P = default_primes()
+    rs = refmod.RefSet.build(P)
+    s = cuboid.SieveSet.build(P)
+    for start in [(152, 3), (153, 7000), (401, 23000), (499, cuboid.q_bounds(499)[1])]:
+        ref = refmod.scan(rs, start[0], start[1], 700, batch_pairs=bp, stop_preset=True)
+        got = cuboid.scan(s, start, 700, opt=cuboid.ScanOptions(batch_pairs=bp, stop=True))
+        assert got.stopped == ref.stopped
+        assert (got.resume_p, got.resume_q) == (ref.resume_p, ref.resume_q)
+        assert got.pairs_tested == ref.pairs_tested and got.survivors == ref.survivors
+        assert got.kill_histogram == ref.kill_histogram(P)
+        assert got.block_r_max == ref.block_r_max
+        tail = cuboid.scan(s, (got.resume_p, got.resume_q), 700)
+        got.merge(tail)
+        whole = refmod.scan(rs, start[0], start[1], 700)
+        assert got.pairs_tested == whole.pairs_tested
+        assert got.kill_histogram == whole.kill_histogram(P)
+        assert got.block_r_max == whole.block_r_max
