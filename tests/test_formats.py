@@ -78,3 +78,20 @@ def test_serialize_rejects_bad_lists():
     for P in ([13, 11], [11, 15], [9697]):
         with pytest.raises(N.CudaSieveError):
             serialize_index(P)
+
+
+def test_is_unsolvable_examples():
+    """test_sievetable.cpp:212-220, through the Python mirror's host accessor
+    (no device needed to read a set's bytes)."""
+    from paper_1601_00636_b200 import cuboid
+    tb, offs = port.build_set([11])
+    s = cuboid.SieveSet([11], tb, offs, 0)
+    assert s.is_unsolvable(0, 1, 2)
+    assert not s.is_unsolvable(0, 12, 21)   # residues (1, 10)
+    assert not s.is_unsolvable(0, 22, 7)    # residue row 0
+    assert s.is_unsolvable(0, 12, 13)       # residues (1, 2)
+    with pytest.raises(IndexError):
+        s.is_unsolvable(3, 1, 2)
+    assert s.prime_count() == 1 and s.prime_at(0) == 11 and s.rank_of(11) == 0 and s.rank_of(13) is None
+    assert s.table_at(0).bytes == tb
+    assert cuboid.dump_table_text(s, 11).splitlines()[0] == "r=11"

@@ -441,3 +441,29 @@ def test_prearmed_stop_matches_reference(bp):
         assert got.pairs_tested == whole.pairs_tested
         assert got.kill_histogram == whole.kill_histogram(P)
         assert got.block_r_max == whole.block_r_max
+
+
+def test_multi_chunk_launch(dev, sets):
+    """A range of more than one launch chunk (1,048,500 row slots): TRIANGLE
+    p <= 1.1e6 (3.7e11 pairs) -- every candidate counted once across the
+    chunked plan/sieve launches, and block-cyclic shards merging to it."""
+    P = sets["odd32"]
+    tb, _ = port.build_set(P)
+    dev.load(P, tb)
+    hi = 1_100_000
+    r = dev.sieve(2, hi, N.TRIANGLE)
+    assert r.pairs_tested == phi_sum(2, hi)
+    assert int(r.hist.sum()) + r.survivors == r.pairs_tested
+    assert (r.block_rmax >= 1).all()
+    parts = [dev.sieve(2, hi, N.TRIANGLE, shard=(2, k)) for k in range(2)]
+    assert sum(x.pairs_tested for x in parts) == r.pairs_tested
+    assert np.array_equal(parts[0].hist + parts[1].hist, r.hist)
+    assert np.array_equal(np.maximum(parts[0].block_rmax, parts[1].block_rmax), r.block_rmax)
+
+
+def test_build_is_deterministic(dev, sets):
+    """test_sievetable.cpp:264-270: building twice gives identical bytes."""
+    for alg in (N.BUILD_PRODUCTION, N.BUILD_EXHAUSTIVE):
+        a, _ = dev.build(sets["odd64"], alg)
+        b, _ = dev.build(sets["odd64"], alg)
+        assert a == b
