@@ -138,6 +138,7 @@ struct cgpu_ctx {
 
 	// probe list
 	uint32_t np = 0, nreg = 0, nreg2 = 0, nreg3 = 0;
+	bool std_primes = false;
 	std::vector<uint32_t> probe_rank, probe_r;
 	DevBuf<uint4> probes;
 	uint32_t reg_r[kMaxReg] = {}, reg_m[kMaxReg] = {}, reg_base[kMaxReg] = {}, reg_delta[kMaxReg] = {};
@@ -364,7 +365,12 @@ int finalize_set(cgpu_ctx* c)
 	const size_t smem = sieve_smem_bytes(c->np);
 	if (smem > 220 * 1024)
 		return set_err(CGPU_ERR_INVALID, "too many probe primes for the sieve's shared memory");
-	c->grid = sieve_grid(c->device, static_cast<int>(c->nreg2), static_cast<int>(c->nreg3), smem);
+	{
+		static const uint32_t std_primes[8] = {11, 13, 17, 19, 23, 29, 31, 37};
+		c->std_primes = c->nreg2 == 7 && c->nreg3 == 1 && !std::getenv("CUBOID_NO_STD_PRIMES");
+		for (uint32_t j = 0; c->std_primes && j < 8; ++j) c->std_primes = c->reg_r[j] == std_primes[j];
+	}
+	c->grid = sieve_grid(c->device, static_cast<int>(c->nreg2), static_cast<int>(c->nreg3), c->std_primes, smem);
 	CK(cudaGetLastError());
 	CK(cudaStreamSynchronize(c->stream));
 	c->loaded = true;
@@ -692,6 +698,7 @@ int enqueue_sieve(cgpu_ctx* c, uint64_t p_lo, uint64_t q_start, uint64_t p_hi, u
 	a.nreg = c->nreg;
 	a.nreg2 = c->nreg2;
 	a.nreg3 = c->nreg3;
+	a.std_primes = c->std_primes;
 	for (int j = 0; j < kMaxReg; ++j) {
 		a.reg_r[j] = c->reg_r[j];
 		a.reg_m[j] = c->reg_m[j];

@@ -73,6 +73,7 @@ struct SieveArgs {
 	uint32_t np;                  // probes (killable tables, rank order)
 	uint32_t nreg;                // leading probes held in registers (nreg2 + nreg3)
 	uint32_t nreg2, nreg3;
+	bool std_primes;              // register probes are exactly 11..31, 37 (immediates)
 	uint32_t reg_r[kMaxReg], reg_m[kMaxReg], reg_base[kMaxReg], reg_delta[kMaxReg];
 	const uint2* fprimes;         // {f, barrett m} primes < 2^16 for trial division
 	uint32_t n_fprimes;
@@ -102,7 +103,7 @@ struct SieveArgs {
 
 cudaError_t launch_plan(const SieveArgs& a, cudaStream_t s);
 cudaError_t launch_sieve(const SieveArgs& a, int grid, cudaStream_t s);
-int sieve_grid(int device, int nr2, int nr3, size_t smem_bytes);
+int sieve_grid(int device, int nr2, int nr3, bool std_primes, size_t smem_bytes);
 __host__ __device__ size_t sieve_smem_bytes(uint32_t np);
 __host__ __device__ inline uint32_t plan_chunks(uint32_t n_slots) { return (n_slots + kPlanChunk - 1) / kPlanChunk; }
 

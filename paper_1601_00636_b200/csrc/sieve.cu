@@ -35,8 +35,35 @@ namespace cgpu {
 namespace {
 
 constexpr uint32_t kFull = 0xffffffffu;
-constexpr uint32_t kDeepPrefetch = 8;  // deep probes whose rows are prefetched per row
 constexpr uint32_t kStepQ = 32 * 32;  // q advance per warp iteration per lane
+constexpr uint32_t kDeepPrefetch = 8;  // deep probes whose rows are prefetched per row
+
+// The register probes of every BASELINE set and of the reference default
+// (sievetable.hpp:178-179): 11..31 and 37. For them the kernel is compiled with
+// the primes, their Barrett constants and per-iteration offset steps as
+// immediates, so the window loop loads nothing from the constant bank.
+__host__ __device__ constexpr uint32_t std_prime(int j)
+{
+	return j == 0 ? 11 : j == 1 ? 13 : j == 2 ? 17 : j == 3 ? 19 : j == 4 ? 23 : j == 5 ? 29 : j == 6 ? 31 : 37;
+}
+
+template <bool STD>
+__device__ __forceinline__ uint32_t reg_prime(const SieveArgs& a, int j)
+{
+	return STD ? std_prime(j) : a.reg_r[j];
+}
+
+template <bool STD>
+__device__ __forceinline__ uint32_t reg_barrett(const SieveArgs& a, int j)
+{
+	return STD ? static_cast<uint32_t>((1ull << 32) / std_prime(j)) : a.reg_m[j];
+}
+
+template <bool STD>
+__device__ __forceinline__ uint32_t reg_step(const SieveArgs& a, int j)
+{
+	return STD ? (kStepQ % std_prime(j)) : a.reg_delta[j];
+}
 
 // least q >= 1 with 9 q^3 >= p (region.hpp:25-39) / q_bounds (region.hpp:49-63)
 __device__ __forceinline__ uint64_t q_low_dev(uint64_t p)
@@ -223,6 +250,7 @@ __device__ __forceinline__ void hist_add(const SieveArgs& a, uint32_t* h, uint32
 struct WarpSmem {
 	uint2* queue;    // [kQueue] windows alive after the register probes: {q0, alive}
 	uint32_t* hist;  // [np] first-kill counts of this warp
+	uint4* deep;     // [kDeepPrefetch] first deep probes of the current row: {row base, r, m, -}
 };
 
 // Warp-aggregated survivor output: one atomic per warp.
@@ -268,10 +296,21 @@ __device__ __forceinline__ uint32_t drain(const SieveArgs& a, const WarpSmem& w,
 		if (!__any_sync(kFull, alive)) break;
 		uint32_t c = 0;
 		if (alive) {
-			// probe j = {r, m, ext_base, S}; row p mod r of its ext table
-			const uint4 d = __ldg(a.probes + j);
-			const uint32_t row = d.z + mod_full(p, d.x, d.y) * d.w;
-			const uint32_t b = mod_full(q0, d.x, d.y);
+			// probe j = {r, m, ext_base, S}; row p mod r of its ext table (the
+			// first kDeepPrefetch were resolved at row setup)
+			uint32_t row, r, m;
+			if (j - NREG < kDeepPrefetch) {
+				const uint4 e = w.deep[j - NREG];
+				row = e.x;
+				r = e.y;
+				m = e.z;
+			} else {
+				const uint4 d = __ldg(a.probes + j);
+				row = d.z + mod_full(p, d.x, d.y) * d.w;
+				r = d.x;
+				m = d.y;
+			}
+			const uint32_t b = mod_full(q0, r, m);
 			const uint32_t* wp = a.ext + row + (b >> 5);
 			CGPU_CHECK(row + (b >> 5) + 1 < a.ext_words);
 			const uint32_t M = __funnelshift_r(__ldg(wp), __ldg(wp + 1), b);
@@ -319,7 +358,7 @@ __device__ __forceinline__ uint32_t coprime_in(const RowCtx& rc, uint32_t lane, 
 // The window loop of one row segment, specialised on the number of odd prime
 // factors NF so the coprimality masks cost exactly NF x 4 instructions.
 // Returns 1 + the deepest probe that killed in this segment (0: none).
-template <int NR2, int NR3, int NF>
+template <int NR2, int NR3, bool STD, int NF>
 __device__ __forceinline__ uint32_t row_loop(const SieveArgs& a, const WarpSmem& w, uint32_t lane,
                                              const RowCtx& rc)
 {
@@ -354,7 +393,7 @@ __device__ __forceinline__ uint32_t row_loop(const SieveArgs& a, const WarpSmem&
 	uint32_t rw2[NR3 > 0 ? NR3 : 1];
 #pragma unroll
 	for (int j = 0; j < NREG; ++j) {
-		const uint32_t r = a.reg_r[j], m = a.reg_m[j];
+		const uint32_t r = reg_prime<STD>(a, j), m = reg_barrett<STD>(a, j);
 		const uint32_t S = j < NR2 ? 2 : 3;
 		const uint32_t row = a.reg_base[j] + mod_full(rc.p, r, m) * S;
 		CGPU_CHECK(row + S - 1 < a.ext_words);
@@ -389,8 +428,8 @@ __device__ __forceinline__ uint32_t row_loop(const SieveArgs& a, const WarpSmem&
 				alive &= ~__funnelshift_r(lo ? rw0[j] : rw1[j], lo ? rw1[j] : rw2[j >= NR2 ? j - NR2 : 0], rb[j]);
 			}
 			if (j + 1 < NREG) S[j + 1] += __popc(alive);
-			const uint32_t t = rb[j] + a.reg_delta[j];
-			rb[j] = min(t, t - a.reg_r[j]);
+			const uint32_t t = rb[j] + reg_step<STD>(a, j);
+			rb[j] = min(t, t - reg_prime<STD>(a, j));
 		}
 		const uint32_t m = __ballot_sync(kFull, alive != 0);
 		if (m) {
@@ -439,7 +478,7 @@ __device__ __forceinline__ uint32_t row_loop(const SieveArgs& a, const WarpSmem&
 	return kmax;
 }
 
-template <int NR2, int NR3>
+template <int NR2, int NR3, bool STD>
 __device__ __forceinline__ uint32_t dispatch_row(const SieveArgs& a, const WarpSmem& w, uint32_t lane,
                                                  const RowCtx& rc)
 {
@@ -451,15 +490,15 @@ __device__ __forceinline__ uint32_t dispatch_row(const SieveArgs& a, const WarpS
 	switch (rc.nf) {
 	case 0:
 	case 1:
-	case 2: return row_loop<NR2, NR3, 2>(a, w, lane, rc);
-	case 3: return row_loop<NR2, NR3, 3>(a, w, lane, rc);
+	case 2: return row_loop<NR2, NR3, STD, 2>(a, w, lane, rc);
+	case 3: return row_loop<NR2, NR3, STD, 3>(a, w, lane, rc);
 	case 4:
-	case 5: return row_loop<NR2, NR3, 5>(a, w, lane, rc);
-	default: return row_loop<NR2, NR3, 9>(a, w, lane, rc);
+	case 5: return row_loop<NR2, NR3, STD, 5>(a, w, lane, rc);
+	default: return row_loop<NR2, NR3, STD, 9>(a, w, lane, rc);
 	}
 }
 
-template <int NR2, int NR3>
+template <int NR2, int NR3, bool STD>
 __global__ void __launch_bounds__(kSieveThreads, kSieveMinBlocks) k_sieve(const SieveArgs a)
 {
 	constexpr int NREG = NR2 + NR3;
@@ -471,7 +510,9 @@ __global__ void __launch_bounds__(kSieveThreads, kSieveMinBlocks) k_sieve(const 
 	WarpSmem w;
 	uint2* q_all = reinterpret_cast<uint2*>(s_dyn);
 	w.queue = q_all + wib * kQueue;
-	uint32_t* h_all = reinterpret_cast<uint32_t*>(q_all + kSieveWarps * kQueue);
+	w.deep = reinterpret_cast<uint4*>(q_all + kSieveWarps * kQueue) + wib * kDeepPrefetch;
+	uint32_t* h_all = reinterpret_cast<uint32_t*>(reinterpret_cast<uint4*>(q_all + kSieveWarps * kQueue) +
+	                                              kSieveWarps * kDeepPrefetch);
 	w.hist = h_all + static_cast<size_t>(wib) * a.np;
 	for (uint32_t j = lane; j < a.np; j += 32) w.hist[j] = 0;
 	__syncwarp();
@@ -534,17 +575,19 @@ __global__ void __launch_bounds__(kSieveThreads, kSieveMinBlocks) k_sieve(const 
 		// q0 parity is fixed per lane (q advances by 32 per window): even p
 		// excludes the even q of every window
 		rc.even = even ? (((rc.qlo + 32 * (rc.w0 + lane)) & 1) ? 0xAAAAAAAAu : 0x55555555u) : 0u;
-#ifndef CGPU_NO_DEEP_PREFETCH
-		// pull the rows of the first deep probes into L1: every drain of this
-		// row walks them first (lanes 2k, 2k+1 take the two lines of probe k)
+		// resolve the rows of the first deep probes (every drain of this row
+		// walks them first) and pull them into L1 (lanes 2k, 2k+1 take the two
+		// lines of probe k)
 		if (NREG + lane / 2 < a.np && lane < 2 * kDeepPrefetch) {
 			const uint4 d = __ldg(a.probes + NREG + lane / 2);
-			const uint32_t* row = a.ext + d.z + mod_full(rc.p, d.x, d.y) * d.w + (lane & 1) * 32;
+			const uint32_t base = d.z + mod_full(rc.p, d.x, d.y) * d.w;
+			if ((lane & 1) == 0) w.deep[lane / 2] = make_uint4(base, d.x, d.y, 0);
+			const uint32_t* row = a.ext + base + (lane & 1) * 32;
 			if ((lane & 1) == 0 || d.w > 32) asm volatile("prefetch.global.L1 [%0];" ::"l"(row));
 		}
-#endif
+		__syncwarp();
 
-		const uint32_t kk = dispatch_row<NR2, NR3>(a, w, lane, rc);  // 1 + deepest killer
+		const uint32_t kk = dispatch_row<NR2, NR3, STD>(a, w, lane, rc);  // 1 + deepest killer
 		if (lane == 0 && kk) {
 			const uint32_t j = kk - 1;
 			const uint32_t killer = j < NREG ? a.reg_r[j < NREG ? j : 0] : __ldg(a.probes + j).x;
@@ -613,16 +656,17 @@ __global__ void k_classify(const uint64_t* __restrict__ pq, uint64_t n,
 	}
 }
 
-template <int NR2, int NR3>
+template <int NR2, int NR3, bool STD = false>
 void* sieve_fn()
 {
-	return reinterpret_cast<void*>(&k_sieve<NR2, NR3>);
+	return reinterpret_cast<void*>(&k_sieve<NR2, NR3, STD>);
 }
 
 // Instantiated: NR2 in 0..8 with NR3 = 0, and NR2 = 7 (every prime 11..31
 // killable -- all BASELINE sets) with NR3 in 1..kMaxReg3.
-void* sieve_kernel_ptr(int nr2, int nr3)
+void* sieve_kernel_ptr(int nr2, int nr3, bool std_primes)
 {
+	if (std_primes) return sieve_fn<7, 1, true>();
 	if (nr2 == 7 && nr3 > 0) {
 		switch (nr3) {
 		case 1: return sieve_fn<7, 1>();
@@ -648,14 +692,15 @@ void* sieve_kernel_ptr(int nr2, int nr3)
 
 __host__ __device__ size_t sieve_smem_bytes(uint32_t np)
 {
-	return sizeof(uint32_t) * static_cast<size_t>(np) * kSieveWarps + sizeof(uint2) * kQueue * kSieveWarps;
+	return sizeof(uint32_t) * static_cast<size_t>(np) * kSieveWarps + sizeof(uint2) * kQueue * kSieveWarps +
+	       sizeof(uint4) * kDeepPrefetch * kSieveWarps;
 }
 
-int sieve_grid(int device, int nr2, int nr3, size_t smem)
+int sieve_grid(int device, int nr2, int nr3, bool std_primes, size_t smem)
 {
 	int sms = 0, per_sm = 0;
 	cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-	const void* fn = sieve_kernel_ptr(nr2, nr3);
+	const void* fn = sieve_kernel_ptr(nr2, nr3, std_primes);
 	if (smem > 48 * 1024)
 		cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
 	cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kSieveThreads, smem);
@@ -673,7 +718,8 @@ cudaError_t launch_sieve(const SieveArgs& a, int grid, cudaStream_t s)
 {
 	const size_t smem = sieve_smem_bytes(a.np);
 	void* args[] = {const_cast<SieveArgs*>(&a)};
-	return cudaLaunchKernel(sieve_kernel_ptr(static_cast<int>(a.nreg2), static_cast<int>(a.nreg3)), dim3(grid),
+	return cudaLaunchKernel(sieve_kernel_ptr(static_cast<int>(a.nreg2), static_cast<int>(a.nreg3), a.std_primes),
+	                        dim3(grid),
 	                        dim3(kSieveThreads), args, smem, s);
 }
 
