@@ -12,18 +12,19 @@
 //   * per p/100 block, the largest killing prime (1 if none) (:229-236, 271).
 //
 // Design: bit-sliced. One lane owns a 32-wide window of
-// consecutive q in one row p; a probe for prime r is ONE funnel shift of two
-// words of the row-extended table (row p mod r, starting at bit q0 mod r),
-// so one probe answers 32 pairs. Warps own contiguous slices of the
-// linearised (row, window) space (k_plan balances them). Per row, a warp
-// trial-divides p once; coprimality is then one periodic bit pattern per odd
-// prime factor (the loop is specialised on the factor count, so no predicated
-// dead slots), plus a constant mask for f = 2. The leading probe primes
-// (r <= 31) live entirely in registers (two words per row). Windows still
-// alive after them (a few percent) are pushed to a per-warp queue in shared
-// memory and probed against the deep tables 32 at a time, one per lane, so
-// the rare deep probes run at full SIMD width. Tables that never kill
-// (all-zero, e.g. r = 3, 5, 7) are not probed -- identical results.
+// consecutive q in one row p; a probe for prime r is ONE funnel shift of the
+// row-extended table (row p mod r, starting at bit q0 mod r), so one probe
+// answers 32 pairs. Warps own contiguous slices of the linearised
+// (row, window) space, balanced by k_plan, which also factorises every p;
+// coprimality is then one periodic bit pattern per odd prime factor (the
+// window loop is specialised on the factor count) plus a constant mask for
+// f = 2. The leading probe primes (11..31, and the first in (31, 63]) live
+// entirely in registers (2-3 words per row) and count their first kills by
+// telescoping popcounts. Windows still alive after them (a few percent) are
+// pushed to a per-warp queue in shared memory and probed against the deep
+// tables 32 at a time, one per lane, so the rare deep probes run at full SIMD
+// width. Tables that never kill (all-zero, e.g. r = 3, 5, 7) are not probed --
+// identical results.
 
 #include <cuda/std/type_traits>
 
@@ -115,8 +116,8 @@ __device__ __forceinline__ uint64_t row_windows(const RowBounds& b)
 }
 
 // Work units of a row for load balancing: its 32-q windows plus a fixed
-// charge a.row_cost for the per-row setup (trial division of p, per-prime row
-// bases, the row-end queue drain). Without it the warps that own the many
+// charge a.row_cost for the per-row setup (factor masks, register-probe rows,
+// the row-end queue drain and counts). Without it the warps that own the many
 // short rows at small p straggle (C4: one SM busy 5x longer than the rest).
 __device__ __forceinline__ uint64_t row_units(const SieveArgs& a, const RowBounds& b)
 {
@@ -225,12 +226,14 @@ __global__ void __launch_bounds__(kPlanChunk) k_plan(const SieveArgs a)
 	}
 }
 
+#ifdef CGPU_DEBUG
 __device__ __forceinline__ uint32_t dynamic_smem_size()
 {
 	uint32_t v;
 	asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(v));
 	return v;
 }
+#endif
 
 __device__ __forceinline__ uint32_t warp_sum(uint32_t v)
 {
@@ -590,7 +593,11 @@ __global__ void __launch_bounds__(kSieveThreads, kSieveMinBlocks) k_sieve(const 
 		const uint32_t kk = dispatch_row<NR2, NR3, STD>(a, w, lane, rc);  // 1 + deepest killer
 		if (lane == 0 && kk) {
 			const uint32_t j = kk - 1;
-			const uint32_t killer = j < NREG ? a.reg_r[j < NREG ? j : 0] : __ldg(a.probes + j).x;
+			uint32_t killer;
+			if constexpr (NREG > 0)
+				killer = j < static_cast<uint32_t>(NREG) ? a.reg_r[j] : __ldg(a.probes + j).x;
+			else
+				killer = __ldg(a.probes + j).x;
 			CGPU_CHECK(rb.p / 100 - a.blk_lo < a.n_blocks);
 			atomicMax(&a.block_rmax[rb.p / 100 - a.blk_lo], killer);
 		}
