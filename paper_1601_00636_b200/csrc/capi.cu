@@ -142,6 +142,7 @@ struct cgpu_ctx {
 	std::vector<uint32_t> probe_rank, probe_r;
 	DevBuf<uint4> probes;
 	uint32_t reg_r[kMaxReg] = {}, reg_m[kMaxReg] = {}, reg_base[kMaxReg] = {}, reg_delta[kMaxReg] = {};
+	uint32_t reg_tab[kMaxReg] = {}, wtab_n = 0;
 	int grid = 0;
 
 	uint32_t row_cost = kDefaultRowCost;
@@ -362,7 +363,14 @@ int finalize_set(cgpu_ctx* c)
 		                   cudaMemcpyHostToDevice, c->stream));
 	}
 	CK(c->hist.ensure(n));
-	const size_t smem = sieve_smem_bytes(c->np);
+	c->wtab_n = 0;
+	// window tables of the leading kTabProbes register probes (sieve.cu row_loop)
+	for (uint32_t j = 0; j < c->nreg && j < static_cast<uint32_t>(kTabProbes); ++j) {
+		c->reg_tab[j] = c->wtab_n;
+		c->wtab_n += c->reg_r[j];
+	}
+	if (c->wtab_n > kTabMax) return set_err(CGPU_ERR_INVALID, "register-probe window tables exceed kTabMax");
+	const size_t smem = sieve_smem_bytes(c->np, c->wtab_n);
 	if (smem > 220 * 1024)
 		return set_err(CGPU_ERR_INVALID, "too many probe primes for the sieve's shared memory");
 	{
@@ -698,12 +706,14 @@ int enqueue_sieve(cgpu_ctx* c, uint64_t p_lo, uint64_t q_start, uint64_t p_hi, u
 	a.nreg = c->nreg;
 	a.nreg2 = c->nreg2;
 	a.nreg3 = c->nreg3;
+	a.wtab_n = c->wtab_n;
 	a.std_primes = c->std_primes;
 	for (int j = 0; j < kMaxReg; ++j) {
 		a.reg_r[j] = c->reg_r[j];
 		a.reg_m[j] = c->reg_m[j];
 		a.reg_base[j] = c->reg_base[j];
 		a.reg_delta[j] = c->reg_delta[j];
+		a.reg_tab[j] = c->reg_tab[j];
 	}
 	a.fprimes = c->fprimes.p;
 	a.n_fprimes = c->n_fprimes;

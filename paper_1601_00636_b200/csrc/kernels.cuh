@@ -50,17 +50,25 @@ constexpr uint32_t kDeriveThreads = 256;
 
 // ---- K2: sieve ---------------------------------------------------------------
 
-constexpr int kSieveThreads = 256;
+#ifndef CGPU_SIEVE_THREADS
+#define CGPU_SIEVE_THREADS 256
+#endif
+constexpr int kSieveThreads = CGPU_SIEVE_THREADS;
 #ifndef CGPU_SIEVE_MIN_BLOCKS
-#define CGPU_SIEVE_MIN_BLOCKS 2
+#define CGPU_SIEVE_MIN_BLOCKS 3
 #endif
 constexpr int kSieveMinBlocks = CGPU_SIEVE_MIN_BLOCKS;  // CTAs per SM the register budget targets
-constexpr uint32_t kDefaultRowCost = 600;                 // window-equivalents per row setup
+constexpr uint32_t kDefaultRowCost = 800;                 // window-equivalents per row setup
 constexpr int kSieveWarps = kSieveThreads / 32;
 constexpr int kMaxReg2 = 8;     // leading probes held in registers with r <= 31 (2-word rows)
 constexpr int kMaxReg3 = 4;     // then with 31 < r <= 63 (3-word rows), after all of 11..31
 constexpr int kMaxReg = kMaxReg2 + kMaxReg3;
 constexpr int kMaxFactors = 9;  // distinct prime factors of p < 2^32
+#ifndef CGPU_TAB_PROBES
+#define CGPU_TAB_PROBES 8
+#endif
+constexpr int kTabProbes = CGPU_TAB_PROBES;  // leading register probes read from a window table
+constexpr uint32_t kTabMax = 400;              // window-table entries per warp (sum of their r)
 constexpr int kQueue = 64;      // per-warp deep-probe work queue entries
 constexpr uint32_t kPlanChunk = 1024;  // row slots per plan CTA
 constexpr uint32_t kFacWords = 1 + kMaxFactors;  // per row slot: nf | even << 8, odd factors
@@ -75,6 +83,8 @@ struct SieveArgs {
 	uint32_t nreg2, nreg3;
 	bool std_primes;              // register probes are exactly 11..31, 37 (immediates)
 	uint32_t reg_r[kMaxReg], reg_m[kMaxReg], reg_base[kMaxReg], reg_delta[kMaxReg];
+	uint32_t reg_tab[kMaxReg];    // first window-table entry of register probe j (prefix sum of r)
+	uint32_t wtab_n;              // window-table entries per warp (sum of register-probe r; 0 if unused)
 	const uint2* fprimes;         // {f, barrett m} primes < 2^16 for trial division
 	uint32_t n_fprimes;
 	// row slots: slot s -> owned block ordinal s/100, p = (blk0 + ord*G)*100 + s%100
@@ -104,7 +114,7 @@ struct SieveArgs {
 cudaError_t launch_plan(const SieveArgs& a, cudaStream_t s);
 cudaError_t launch_sieve(const SieveArgs& a, int grid, cudaStream_t s);
 int sieve_grid(int device, int nr2, int nr3, bool std_primes, size_t smem_bytes);
-__host__ __device__ size_t sieve_smem_bytes(uint32_t np);
+__host__ __device__ size_t sieve_smem_bytes(uint32_t np, uint32_t wtab_n);
 __host__ __device__ inline uint32_t plan_chunks(uint32_t n_slots) { return (n_slots + kPlanChunk - 1) / kPlanChunk; }
 
 cudaError_t launch_init_blocks(uint32_t* d_block_rmax, uint64_t nblocks, uint64_t blk_lo,
