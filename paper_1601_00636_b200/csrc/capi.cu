@@ -7,6 +7,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <fstream>
+#include <map>
 #include <string>
 #include <vector>
 
@@ -144,6 +145,7 @@ struct cgpu_ctx {
 	uint32_t reg_r[kMaxReg] = {}, reg_m[kMaxReg] = {}, reg_base[kMaxReg] = {}, reg_delta[kMaxReg] = {};
 	uint32_t reg_tab[kMaxReg] = {}, wtab_n = 0;
 	int grid = 0;
+	std::map<uint64_t, int> grid_cache;
 
 	uint32_t row_cost = kDefaultRowCost;
 	DevBuf<uint2> fprimes;
@@ -292,7 +294,9 @@ std::vector<PrimeJob> make_jobs(const std::vector<uint32_t>& primes,
 
 // After the packed bytes are resident: derive ext rows + killable flags, then
 // build the probe list (killable tables in rank order).
-int finalize_set(cgpu_ctx* c)
+// check_padding: a k_check_padding flag was enqueued into killflags[n]; it
+// is read back with the killable flags (one host sync per load).
+int finalize_set(cgpu_ctx* c, bool check_padding = false)
 {
 	const uint32_t n = static_cast<uint32_t>(c->primes.size());
 	std::vector<PrimeJob> jobs = make_jobs(c->primes, c->offsets, c->ext_base, c->ext_words);
@@ -300,7 +304,7 @@ int finalize_set(cgpu_ctx* c)
 		return set_err(CGPU_ERR_OVERFLOW, "row-extended layout exceeds 2^32 words");
 	CK(c->jobs_rank.ensure(n));
 	CK(c->ext.ensure(c->ext_words));
-	CK(c->killflags.ensure(n));
+	CK(c->killflags.ensure(n + 1));
 	CK(c->d_primes.ensure(n));
 	CK(c->d_offsets.ensure(n));
 	if (n) {
@@ -315,9 +319,11 @@ int finalize_set(cgpu_ctx* c)
 		CK(launch_derive(c->jobs_rank.p, n, max_words, c->packed.p, c->ext.p, c->killflags.p, c->stream));
 		++c->launches;
 	}
-	std::vector<uint32_t> kf(n);
-	if (n) CK(cudaMemcpyAsync(kf.data(), c->killflags.p, 4ull * n, cudaMemcpyDeviceToHost, c->stream));
+	std::vector<uint32_t> kf(n + 1, 0);
+	const uint32_t nread = n + (check_padding ? 1 : 0);
+	if (nread) CK(cudaMemcpyAsync(kf.data(), c->killflags.p, 4ull * nread, cudaMemcpyDeviceToHost, c->stream));
 	CK(cudaStreamSynchronize(c->stream));
+	if (check_padding && kf[n]) return set_err(CGPU_ERR_FORMAT, "unpack_bits: nonzero padding bits");
 	c->killable.assign(n, 0);
 	c->probe_rank.clear();
 	c->probe_r.clear();
@@ -378,7 +384,15 @@ int finalize_set(cgpu_ctx* c)
 		c->std_primes = c->nreg2 == 7 && c->nreg3 == 1 && !std::getenv("CUBOID_NO_STD_PRIMES");
 		for (uint32_t j = 0; c->std_primes && j < 8; ++j) c->std_primes = c->reg_r[j] == std_primes[j];
 	}
-	c->grid = sieve_grid(c->device, static_cast<int>(c->nreg2), static_cast<int>(c->nreg3), c->std_primes, smem);
+	{  // occupancy per kernel variant and shared-memory size, computed once per context
+		const uint64_t key = (uint64_t(c->nreg2) << 56) | (uint64_t(c->nreg3) << 48) |
+		                     (uint64_t(c->std_primes) << 40) | smem;
+		auto it = c->grid_cache.find(key);
+		if (it == c->grid_cache.end())
+			it = c->grid_cache.emplace(key, sieve_grid(c->device, static_cast<int>(c->nreg2),
+			                                           static_cast<int>(c->nreg3), c->std_primes, smem)).first;
+		c->grid = it->second;
+	}
 	CK(cudaGetLastError());
 	CK(cudaStreamSynchronize(c->stream));
 	c->loaded = true;
@@ -395,7 +409,7 @@ int begin_set(cgpu_ctx* c, const uint32_t* primes, uint32_t n)
 	c->primes.assign(primes, primes + n);
 	c->offsets = offs;
 	c->total_bytes = total;
-	CK(c->packed.ensure(total));
+	CK(c->packed.ensure(total + 8));  // k_derive reads aligned words one past the last byte
 	return CGPU_OK;
 }
 
@@ -482,17 +496,12 @@ int cgpu_tables_load(cgpu_ctx* c, const uint32_t* primes, uint32_t n, const uint
 		CK(c->jobs_rank.ensure(n));
 		CK(cudaMemcpyAsync(c->jobs_rank.p, jobs.data(), sizeof(PrimeJob) * n, cudaMemcpyHostToDevice,
 		                   c->stream));
-		CK(c->evals.ensure(1));
-		CK(cudaMemsetAsync(c->evals.p, 0, 8, c->stream));
-		CK(launch_check_padding(c->jobs_rank.p, n, c->packed.p,
-		                        reinterpret_cast<uint32_t*>(c->evals.p), c->stream));
+		CK(c->killflags.ensure(n + 1));
+		CK(cudaMemsetAsync(c->killflags.p + n, 0, 4, c->stream));
+		CK(launch_check_padding(c->jobs_rank.p, n, c->packed.p, c->killflags.p + n, c->stream));
 		++c->launches;
-		uint32_t bad = 0;
-		CK(cudaMemcpyAsync(&bad, c->evals.p, 4, cudaMemcpyDeviceToHost, c->stream));
-		CK(cudaStreamSynchronize(c->stream));
-		if (bad) return set_err(CGPU_ERR_FORMAT, "unpack_bits: nonzero padding bits");
 	}
-	return finalize_set(c);
+	return finalize_set(c, n > 0);
 }
 
 int cgpu_tables_download(cgpu_ctx* c, uint8_t* out, uint64_t cap)

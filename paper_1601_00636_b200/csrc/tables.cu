@@ -235,17 +235,32 @@ __global__ void __launch_bounds__(kDeriveThreads) k_derive(const PrimeJob* __res
 	const uint8_t* tab = packed + job.byte_off;
 	const uint32_t mS = barrett_m(S);
 	bool any = false;
+	// 32 bits of the packed bitstream starting at bit i (any alignment), from
+	// the two aligned little-endian words around it
+	const uint64_t base_bits = 8ull * job.byte_off;
+	const uint32_t* words32 = reinterpret_cast<const uint32_t*>(packed);
+	auto bits32 = [&](uint64_t i) {
+		const uint64_t g = base_bits + i;
+		return __funnelshift_r(__ldg(words32 + (g >> 5)), __ldg(words32 + (g >> 5) + 1), static_cast<uint32_t>(g & 31));
+	};
 	for (uint32_t w = blockIdx.x * blockDim.x + threadIdx.x; w < words; w += gridDim.x * blockDim.x) {
 		uint32_t a = __umulhi(w, mS), j = w - a * S;  // w / S, w % S
 		if (j >= S) { j -= S; ++a; }
 		uint32_t b = mod_full(32 * j, r, m);  // offset of bit 0 of the word in the row
 		const uint32_t row0 = a * r;
-		uint32_t word = 0;
+		uint32_t word;
+		if (r >= 32) {  // at most one wrap: bits [b, r) then [0, 32 - (r - b))
+			const uint32_t head = r - b;
+			word = bits32(row0 + b);
+			if (head < 32) word = (word & ((1u << head) - 1)) | (bits32(row0) << head);
+		} else {  // small r: the row repeats inside one word
+			word = 0;
 #pragma unroll 8
-		for (uint32_t l = 0; l < 32; ++l) {
-			const uint32_t idx = row0 + b;
-			word |= ((__ldg(tab + (idx >> 3)) >> (idx & 7)) & 1u) << l;
-			b = b + 1 == r ? 0 : b + 1;
+			for (uint32_t l = 0; l < 32; ++l) {
+				const uint32_t idx = row0 + b;
+				word |= ((__ldg(tab + (idx >> 3)) >> (idx & 7)) & 1u) << l;
+				b = b + 1 == r ? 0 : b + 1;
+			}
 		}
 		ext[job.ext_base + w] = word;
 		any |= word != 0;
