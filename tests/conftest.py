@@ -18,6 +18,13 @@ GOLDEN_PATH = os.path.join(ROOT, "tests", "golden", "golden.json")
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200, sm_100a)")
     config.addinivalue_line("markers", "slow: long-running CPU oracle case")
+    # a fresh checkout has no built libraries (they are not committed): build
+    # them once, here, the same way the driver's build() does
+    libs = [os.path.join(ROOT, "paper_1601_00636_b200", "libcuboid_gpu.so"),
+            os.path.join(ROOT, "oracle", "libcuboid_oracle.so")]
+    if not all(os.path.exists(p) for p in libs):
+        import __graft_entry__
+        __graft_entry__.build()
 
 
 @pytest.fixture(scope="session")
