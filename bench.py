@@ -429,6 +429,17 @@ def run_ours(args, wl, primes):
             traffic = json.load(open(prof)).get("k_sieve", {}).get(wl["desc"][:2], {}).get("dram_bytes")
         except (ValueError, AttributeError):
             traffic = None
+    ncu = None
+    if os.path.exists(prof):
+        try:
+            x = json.load(open(prof)).get("k_sieve", {}).get(wl["desc"][:2], {})
+            ncu = {k: x.get(k) for k in ("round", "duration_ms", "issue_active_pct", "alu_pipe_pct",
+                                          "xu_pipe_pct", "lsu_pipe_pct", "l1tex_throughput_pct",
+                                          "fma_pipe_pct", "warps_active_pct", "registers")}
+            if x.get("duration_ms"):
+                ncu["dram_gbs"] = x.get("dram_bytes", 0) / (x["duration_ms"] * 1e-3) / 1e9
+        except (ValueError, AttributeError):
+            ncu = None
     roof = {"bound": "int32", "achieved": achieved, "peak": int_peak["best"],
             "unit": "INT32 ops/s", "frac": achieved / int_peak["best"], "traffic": traffic,
             "kernel": "k_sieve", "kernel_ms": kavg, "ops_per_pair": opp, "d_eff": d_eff,
@@ -436,6 +447,7 @@ def run_ours(args, wl, primes):
             "peak_source": "measured in this run: best of cgpu_int32_peak's INT32 chains "
                            "(nominal issue limit 148 SM x 128 lanes x clock = 3.72e13 at 1965 MHz)",
             "int32_peaks": int_peak,
+            "ncu_pipes": ncu,
             "note": "ops_per_pair is the reference algorithm's count (SURVEY 8(d)); the kernel "
                     "is bit-sliced (one probe answers 32 q), so frac can exceed 1"}
 

@@ -453,6 +453,39 @@ def scan_triangle(set_: SieveSet, p_lo: int, p_hi: int, sink: Optional[Callable]
     return st
 
 
+@dataclass
+class SmallRegionSummary:
+    """engine.hpp:597-604."""
+    pairs: int = 0
+    sieved_out: int = 0
+    survivors: int = 0
+    no_integer_root: int = 0
+    root_fails: int = 0
+    candidates: int = 0
+
+
+def verify_small_region(set_: SieveSet, verifier: Optional[Callable] = None) -> SmallRegionSummary:
+    """verify_small_region (engine.hpp:609-640): every coprime p != q pair of
+    the region rows p <= 151, sieved on the GPU; survivors go to `verifier`
+    (p, q) -> "NoIntegerRoot" | "RootFailsInequalities" | "CuboidCandidate"
+    (the reference's exact check). A candidate raises, as in the reference."""
+    if set_.empty():
+        raise ValueError("verify_small_region: empty sieve set")
+    st = scan(set_, (1, 1), 151, opt=ScanOptions(small_p=True))
+    out = SmallRegionSummary(pairs=st.pairs_tested, sieved_out=st.pairs_tested - st.survivors,
+                             survivors=st.survivors)
+    for p, q in st.survivor_pairs:
+        kind = verifier(p, q) if verifier else "NoIntegerRoot"
+        if kind == "CuboidCandidate":
+            out.candidates += 1
+            raise RuntimeError(f"cuboid candidate found at p={p}, q={q}")
+        if kind == "RootFailsInequalities":
+            out.root_fails += 1
+        else:
+            out.no_integer_root += 1
+    return out
+
+
 def classify(set_: SieveSet, pairs) -> np.ndarray:
     """First-killer rank per (p, q), -1 if no table rejects it (the sieve part
     of verify_pair, engine.hpp:72-78)."""

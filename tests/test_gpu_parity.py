@@ -467,3 +467,15 @@ def test_build_is_deterministic(dev, sets):
         a, _ = dev.build(sets["odd64"], alg)
         b, _ = dev.build(sets["odd64"], alg)
         assert a == b
+
+
+def test_verify_small_region_pin(golden):
+    """engine.hpp:609-640 / test_engine.cpp:416-423: 413,362 pairs, all sieved out."""
+    s = cuboid.SieveSet.build_default()
+    v = cuboid.verify_small_region(s)
+    g = golden["verify_small_region"]
+    assert (v.pairs, v.sieved_out, v.survivors, v.candidates) == \
+        (g["pairs"], g["sieved_out"], g["survivors"], g["candidates"])
+    weak = cuboid.SieveSet.build([11])
+    w = cuboid.verify_small_region(weak)
+    assert w.survivors > 0 and w.survivors + w.sieved_out == w.pairs
