@@ -46,6 +46,8 @@ WORKLOADS = {
                desc="C5: TRIANGLE sieve 1e5<p<=3e5, 1<=q<p coprime, 256 odd primes 3..1621"),
     "C4": dict(k=128, p_lo=2, p_hi=100000, pairs=3039650753,
                desc="C4: TRIANGLE sieve p<=1e5, 1<=q<p coprime, 128 odd primes 3..727"),
+    "C1": dict(k=32, p_lo=2, p_hi=2000, pairs=1216587,
+               desc="C1: TRIANGLE sieve p<=2000, 1<=q<p coprime, 32 odd primes 3..137"),
     "C3": dict(k=64, p_lo=2, p_hi=10000, pairs=30397485,
                desc="C3: TRIANGLE sieve p<=1e4, 1<=q<p coprime, 64 odd primes 3..313"),
 }
@@ -315,6 +317,20 @@ def run_ours(args, wl, primes):
             "pin_ok": r.survivors == 0 and hk == 137,
         }
 
+    # ---- the other BASELINE sieve configs, one GPU, device time ----------------------
+    other = {}
+    if world == 1:
+        for name in ("C1", "C3", "C4"):
+            o = WORKLOADS[name]
+            dev.build(odd_primes(o["k"]), N.BUILD_PRODUCTION, download=False)
+            ms = []
+            for _ in range(4):
+                r = dev.sieve(o["p_lo"], o["p_hi"], N.TRIANGLE, surv_cap=1 << 16)
+                ms.append(dev.timings_ms()["total"])
+            other[name] = {"workload": o["desc"], "pairs": r.pairs_tested,
+                           "parity": r.pairs_tested == o["pairs"] and r.survivors == 0,
+                           "ms": min(ms[1:]), "pairs_per_s": r.pairs_tested / (min(ms[1:]) * 1e-3)}
+
     # ---- resident set for the workload ------------------------------------------------
     tables, _ = dev.build(primes, N.BUILD_PRODUCTION)
     killable = dev.killable()
@@ -473,6 +489,7 @@ def run_ours(args, wl, primes):
             "roofline": roof,
             "table_build": table_build,
             "historical_region_scan": historical,
+            "other_configs": other or None,
             "clocks": clk.summary(),
         }
         if world == 1 and not args.no_cpu_baseline:
