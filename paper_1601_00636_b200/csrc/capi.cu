@@ -144,6 +144,8 @@ struct cgpu_ctx {
 	DevBuf<uint4> probes;
 	uint32_t reg_r[kMaxReg] = {}, reg_m[kMaxReg] = {}, reg_base[kMaxReg] = {}, reg_delta[kMaxReg] = {};
 	uint32_t reg_tab[kMaxReg] = {}, wtab_n = 0;
+	DevBuf<uint4> d_tabprobes;
+	DevBuf<uint32_t> wintab;
 	int grid = 0;
 	std::map<uint64_t, int> grid_cache;
 
@@ -370,20 +372,37 @@ int finalize_set(cgpu_ctx* c, bool check_padding = false)
 	}
 	CK(c->hist.ensure(n));
 	c->wtab_n = 0;
-	// window tables of the leading kTabProbes register probes (sieve.cu row_loop)
-	for (uint32_t j = 0; j < c->nreg && j < static_cast<uint32_t>(kTabProbes); ++j) {
-		c->reg_tab[j] = c->wtab_n;
-		c->wtab_n += c->reg_r[j];
+	// window tables of the leading kTabProbes register probes, every row
+	// (sieve.cu row_loop): sum of r^2 entries, built on the device
+	{
+		std::vector<uint4> tp;
+		for (uint32_t j = 0; j < c->nreg && j < static_cast<uint32_t>(kTabProbes); ++j) {
+			const uint32_t r = c->reg_r[j];
+			c->reg_tab[j] = c->wtab_n;
+			tp.push_back(make_uint4(r, c->reg_base[j], ext_row_words(r), c->wtab_n));
+			c->wtab_n += r * r;
+		}
+		if (c->wtab_n > kTabStrideGen)
+			return set_err(CGPU_ERR_INVALID, "register-probe window tables exceed kTabStrideGen");
+		CK(c->d_tabprobes.ensure(tp.size()));
+		CK(c->wintab.ensure(2 * kTabStrideGen));
+		if (!tp.empty()) {
+			CK(cudaMemcpyAsync(c->d_tabprobes.p, tp.data(), sizeof(uint4) * tp.size(), cudaMemcpyHostToDevice,
+			                   c->stream));
+			CK(launch_wintab(c->d_tabprobes.p, static_cast<uint32_t>(tp.size()), c->wtab_n, c->ext.p,
+			                 kTabStrideGen, c->wintab.p, c->stream));
+			++c->launches;
+		}
 	}
-	if (c->wtab_n > kTabMax) return set_err(CGPU_ERR_INVALID, "register-probe window tables exceed kTabMax");
-	const size_t smem = sieve_smem_bytes(c->np, c->wtab_n);
-	if (smem > 220 * 1024)
-		return set_err(CGPU_ERR_INVALID, "too many probe primes for the sieve's shared memory");
 	{
 		static const uint32_t std_primes[8] = {11, 13, 17, 19, 23, 29, 31, 37};
 		c->std_primes = c->nreg2 == 7 && c->nreg3 == 1 && !std::getenv("CUBOID_NO_STD_PRIMES");
 		for (uint32_t j = 0; c->std_primes && j < 8; ++j) c->std_primes = c->reg_r[j] == std_primes[j];
 	}
+	const size_t smem =
+	    sieve_smem_bytes(c->np, c->wtab_n ? (c->std_primes ? kTabStrideStd : kTabStrideGen) : 0);
+	if (smem > 220 * 1024)
+		return set_err(CGPU_ERR_INVALID, "too many probe primes for the sieve's shared memory");
 	{  // occupancy per kernel variant and shared-memory size, computed once per context
 		const uint64_t key = (uint64_t(c->nreg2) << 56) | (uint64_t(c->nreg3) << 48) |
 		                     (uint64_t(c->std_primes) << 40) | smem;
@@ -716,6 +735,7 @@ int enqueue_sieve(cgpu_ctx* c, uint64_t p_lo, uint64_t q_start, uint64_t p_hi, u
 	a.nreg2 = c->nreg2;
 	a.nreg3 = c->nreg3;
 	a.wtab_n = c->wtab_n;
+	a.wintab = c->wintab.p;
 	a.std_primes = c->std_primes;
 	for (int j = 0; j < kMaxReg; ++j) {
 		a.reg_r[j] = c->reg_r[j];

@@ -34,6 +34,12 @@ cudaError_t launch_permute(const PrimeJob* d_jobs, uint32_t njobs, uint32_t max_
 
 // Packed reference bytes -> row-extended words + killable flags; jobs in rank
 // order (killable index = blockIdx.y). max_words = largest r * ext_row_words(r).
+// Window tables of the table probes (k_sieve's first kTabProbes register
+// probes) for every row: probes[j] = {r, ext_base, S, tab base}; out holds
+// `stride` masks then `stride` successor indices.
+cudaError_t launch_wintab(const uint4* d_probes, uint32_t nprobes, uint32_t entries, const uint32_t* d_ext,
+                          uint32_t stride, uint32_t* d_out, cudaStream_t s);
+
 cudaError_t launch_derive(const PrimeJob* d_jobs, uint32_t njobs, uint64_t max_words,
                           const uint8_t* d_packed, uint32_t* d_ext, uint32_t* d_killable,
                           cudaStream_t s);
@@ -68,7 +74,11 @@ constexpr int kMaxFactors = 9;  // distinct prime factors of p < 2^32
 #define CGPU_TAB_PROBES 8
 #endif
 constexpr int kTabProbes = CGPU_TAB_PROBES;  // leading register probes read from a window table
-constexpr uint32_t kTabMax = 400;              // window-table entries per warp (sum of their r)
+// Window tables of the table probes, all rows: sum over them of r^2 entries.
+// The 8 standard primes 11..37 need 4640; any admissible 8 table probes fit
+// 7424 (11..31 and one prime below 64: 3271 + 61^2 = 6992).
+constexpr uint32_t kTabStrideStd = 4640;
+constexpr uint32_t kTabStrideGen = 7424;
 constexpr int kQueue = 64;      // per-warp deep-probe work queue entries
 constexpr uint32_t kPlanChunk = 1024;  // row slots per plan CTA
 constexpr uint32_t kFacWords = 1 + kMaxFactors;  // per row slot: nf | even << 8, odd factors
@@ -83,8 +93,10 @@ struct SieveArgs {
 	uint32_t nreg2, nreg3;
 	bool std_primes;              // register probes are exactly 11..31, 37 (immediates)
 	uint32_t reg_r[kMaxReg], reg_m[kMaxReg], reg_base[kMaxReg], reg_delta[kMaxReg];
-	uint32_t reg_tab[kMaxReg];    // first window-table entry of register probe j (prefix sum of r)
-	uint32_t wtab_n;              // window-table entries per warp (sum of register-probe r; 0 if unused)
+	uint32_t reg_tab[kMaxReg];    // first window-table entry of table probe j (prefix sum of r^2)
+	uint32_t wtab_n;              // window-table entries (0: no table probes)
+	const uint32_t* wintab;       // [2][stride]: entry (j, a, b) = mask of row a at offset b, then
+	                              // the successor entry index (a, (b + 1024) mod r)
 	const uint2* fprimes;         // {f, barrett m} primes < 2^16 for trial division
 	uint32_t n_fprimes;
 	// row slots: slot s -> owned block ordinal s/100, p = (blk0 + ord*G)*100 + s%100
@@ -114,7 +126,7 @@ struct SieveArgs {
 cudaError_t launch_plan(const SieveArgs& a, cudaStream_t s);
 cudaError_t launch_sieve(const SieveArgs& a, int grid, cudaStream_t s);
 int sieve_grid(int device, int nr2, int nr3, bool std_primes, size_t smem_bytes);
-__host__ __device__ size_t sieve_smem_bytes(uint32_t np, uint32_t wtab_n);
+__host__ __device__ size_t sieve_smem_bytes(uint32_t np, uint32_t tab_stride);
 __host__ __device__ inline uint32_t plan_chunks(uint32_t n_slots) { return (n_slots + kPlanChunk - 1) / kPlanChunk; }
 
 cudaError_t launch_init_blocks(uint32_t* d_block_rmax, uint64_t nblocks, uint64_t blk_lo,

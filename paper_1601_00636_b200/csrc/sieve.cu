@@ -256,7 +256,7 @@ struct WarpSmem {
 	uint2* queue;    // [kQueue] windows alive after the register probes: {q0, alive}
 	uint32_t* hist;  // [np] first-kill counts of this warp
 	uint4* deep;     // [kDeepPrefetch] first deep probes of the current row: {row base, r, m, -}
-	uint32_t* wintab;  // [2 * kTabMax] window table of the current row: masks, then successors
+	uint32_t tab0;   // shared address of the CTA's window tables (masks; successors TS words on)
 };
 
 // Warp-aggregated survivor output: one atomic per warp.
@@ -369,7 +369,8 @@ __device__ __forceinline__ uint32_t row_loop(const SieveArgs& a, const WarpSmem&
                                              const RowCtx& rc)
 {
 	constexpr int NREG = NR2 + NR3;  // register probes: NR2 with r <= 31, NR3 with 31 < r <= 63
-	constexpr int NT = NREG < kTabProbes ? NREG : kTabProbes;  // probes read from the window table
+	constexpr int NT = NREG < kTabProbes ? NREG : kTabProbes;  // probes read from the window tables
+	constexpr uint32_t TS = STD ? kTabStrideStd : kTabStrideGen;
 	// S[j] = sum over this lane's windows of popc(alive before register probe j);
 	// probe j's first-kill count is S[j] - S[j+1] (telescoping: one LOP3 per
 	// probe). S[0] (the candidates) is counted once per segment by
@@ -411,32 +412,17 @@ __device__ __forceinline__ uint32_t row_loop(const SieveArgs& a, const WarpSmem&
 		if (j >= NR2) rw2[j >= NR2 ? j - NR2 : 0] = __ldg(a.ext + row + 2);
 		rb[j] = mod_full(q0_first, r, m);
 	}
-	// Register probes j < NT: a per-warp window table in shared memory. Entry
-	// (j, b) holds the 32-q window of prime j's row at offset b; its successor
-	// entry (the lane's next offset, (b + 1024) mod r) is stored kTabMax words
-	// further, so a probe is two LDS.32 -- no funnel shift, no offset update.
+	// Register probes j < NT: the window tables of every row of these primes
+	// are resident in the CTA's shared memory (copied once per launch). Entry
+	// (j, a, b) holds the 32-q mask of row a at offset b; the shared address of
+	// the lane's next entry, (a, (b + 1024) mod r), sits TS words further, so a
+	// probe is two LDS.32 -- no funnel shift, no offset update, no per-row setup
+	// beyond locating the lane's first entry.
 	uint32_t ta[NT > 0 ? NT : 1];  // shared address of this lane's current entry
-	if constexpr (NT > 0) {
-		const uint32_t tab0 = static_cast<uint32_t>(__cvta_generic_to_shared(w.wintab));
-		for (uint32_t e = lane; e < a.wtab_n; e += 32) {
-			int jj = 0;
 #pragma unroll
-			for (int j = 1; j < NT; ++j)
-				if (e >= a.reg_tab[j]) jj = j;
-			const uint32_t r = a.reg_r[jj], m = a.reg_m[jj], S = jj < NR2 ? 2 : 3;
-			const uint32_t b = e - a.reg_tab[jj];
-			const uint32_t* row = a.ext + a.reg_base[jj] + mod_full(rc.p, r, m) * S;
-			const uint32_t k = b >> 5;  // 0, or 1 for 3-word rows
-			const uint32_t t = b + a.reg_delta[jj];
-			w.wintab[e] = __funnelshift_r(__ldg(row + k), __ldg(row + k + 1), b);
-			w.wintab[kTabMax + e] = tab0 + 4 * (a.reg_tab[jj] + min(t, t - r));
-		}
-#pragma unroll
-		for (int j = 0; j < NT; ++j) {
-			const uint32_t r = reg_prime<STD>(a, j), m = reg_barrett<STD>(a, j);
-			ta[j] = tab0 + 4 * (a.reg_tab[j] + mod_full(q0_first, r, m));
-		}
-		__syncwarp();
+	for (int j = 0; j < NT; ++j) {
+		const uint32_t r = reg_prime<STD>(a, j), m = reg_barrett<STD>(a, j);
+		ta[j] = w.tab0 + 4 * (a.reg_tab[j] + mod_full(rc.p, r, m) * r + mod_full(q0_first, r, m));
 	}
 	const uint32_t lt = (1u << lane) - 1;
 	uint32_t qn = 0;  // queued windows
@@ -460,7 +446,7 @@ __device__ __forceinline__ uint32_t row_loop(const SieveArgs& a, const WarpSmem&
 			if (j < NT) {
 				uint32_t M, nx;
 				asm volatile("ld.shared.u32 %0, [%1];" : "=r"(M) : "r"(ta[j < NT ? j : 0]));
-				asm volatile("ld.shared.u32 %0, [%1+%2];" : "=r"(nx) : "r"(ta[j < NT ? j : 0]), "n"(4 * kTabMax));
+				asm volatile("ld.shared.u32 %0, [%1+%2];" : "=r"(nx) : "r"(ta[j < NT ? j : 0]), "n"(4 * TS));
 				alive &= ~M;
 				ta[j < NT ? j : 0] = nx;
 			} else {
@@ -555,16 +541,22 @@ __global__ void __launch_bounds__(kSieveThreads, kSieveMinBlocks) k_sieve(const 
 	uint2* q_all = reinterpret_cast<uint2*>(s_dyn);
 	w.queue = q_all + wib * kQueue;
 	w.deep = reinterpret_cast<uint4*>(q_all + kSieveWarps * kQueue) + wib * kDeepPrefetch;
-	uint32_t* t_all = reinterpret_cast<uint32_t*>(reinterpret_cast<uint4*>(q_all + kSieveWarps * kQueue) +
+	uint32_t* h_all = reinterpret_cast<uint32_t*>(reinterpret_cast<uint4*>(q_all + kSieveWarps * kQueue) +
 	                                              kSieveWarps * kDeepPrefetch);
-	const uint32_t tab_words = a.wtab_n ? 2 * kTabMax : 0;
-	w.wintab = t_all + static_cast<size_t>(wib) * tab_words;
-	uint32_t* h_all = t_all + static_cast<size_t>(kSieveWarps) * tab_words;
 	w.hist = h_all + static_cast<size_t>(wib) * a.np;
 	for (uint32_t j = lane; j < a.np; j += 32) w.hist[j] = 0;
-	__syncwarp();
+	// the window tables, resident for the whole launch: masks, then successor
+	// entries as shared addresses
+	constexpr uint32_t TS = STD ? kTabStrideStd : kTabStrideGen;
+	uint32_t* s_tab = h_all + static_cast<size_t>(kSieveWarps) * a.np;
+	w.tab0 = static_cast<uint32_t>(__cvta_generic_to_shared(s_tab));
+	for (uint32_t e = threadIdx.x; e < a.wtab_n; e += blockDim.x) {
+		s_tab[e] = __ldg(a.wintab + e);
+		s_tab[TS + e] = w.tab0 + 4 * __ldg(a.wintab + kTabStrideGen + e);
+	}
+	__syncthreads();
 
-	CGPU_CHECK(sieve_smem_bytes(a.np, a.wtab_n) <= dynamic_smem_size());
+	CGPU_CHECK(sieve_smem_bytes(a.np, a.wtab_n ? TS : 0) <= dynamic_smem_size());
 	const uint32_t n_chunks = plan_chunks(a.n_slots);
 	const unsigned long long W = a.chunk_off[n_chunks];
 	const unsigned long long nwarps = static_cast<unsigned long long>(gridDim.x) * kSieveWarps;
@@ -741,10 +733,10 @@ void* sieve_kernel_ptr(int nr2, int nr3, bool std_primes)
 
 }  // namespace
 
-__host__ __device__ size_t sieve_smem_bytes(uint32_t np, uint32_t wtab_n)
+__host__ __device__ size_t sieve_smem_bytes(uint32_t np, uint32_t tab_stride)
 {
 	return sizeof(uint32_t) * static_cast<size_t>(np) * kSieveWarps + sizeof(uint2) * kQueue * kSieveWarps +
-	       sizeof(uint4) * kDeepPrefetch * kSieveWarps + (wtab_n ? sizeof(uint32_t) * 2 * kTabMax * kSieveWarps : 0);
+	       sizeof(uint4) * kDeepPrefetch * kSieveWarps + sizeof(uint32_t) * 2 * tab_stride;
 }
 
 int sieve_grid(int device, int nr2, int nr3, bool std_primes, size_t smem)
@@ -767,7 +759,7 @@ cudaError_t launch_plan(const SieveArgs& a, cudaStream_t s)
 
 cudaError_t launch_sieve(const SieveArgs& a, int grid, cudaStream_t s)
 {
-	const size_t smem = sieve_smem_bytes(a.np, a.wtab_n);
+	const size_t smem = sieve_smem_bytes(a.np, a.wtab_n ? (a.std_primes ? kTabStrideStd : kTabStrideGen) : 0);
 	void* args[] = {const_cast<SieveArgs*>(&a)};
 	return cudaLaunchKernel(sieve_kernel_ptr(static_cast<int>(a.nreg2), static_cast<int>(a.nreg3), a.std_primes),
 	                        dim3(grid),

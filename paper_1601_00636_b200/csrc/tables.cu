@@ -268,6 +268,25 @@ __global__ void __launch_bounds__(kDeriveThreads) k_derive(const PrimeJob* __res
 	if (__any_sync(kFull, any) && (threadIdx.x & 31) == 0) atomicOr(&killable[blockIdx.y], 1u);
 }
 
+// Window tables for the sieve's table probes: entry (j, a, b) -- for probe j
+// (prime r), row a = p mod r, offset b -- is the 32-q mask of that row at b
+// (bits u(a, (b + l) mod r)), and the entry index of the lane's next window
+// (a, (b + 1024) mod r). One thread per entry.
+__global__ void k_wintab(const uint4* __restrict__ probes, uint32_t nprobes, uint32_t entries,
+                         const uint32_t* __restrict__ ext, uint32_t stride, uint32_t* __restrict__ out)
+{
+	for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < entries; e += gridDim.x * blockDim.x) {
+		uint32_t j = 0;
+		while (j + 1 < nprobes && e >= probes[j + 1].w) ++j;
+		const uint4 d = probes[j];  // {r, ext_base, S, base}
+		const uint32_t r = d.x, i = e - d.w, a = i / r, b = i - a * r;
+		const uint32_t* row = ext + d.y + a * d.z;
+		const uint32_t k = b >> 5;  // 0, or 1 for 3-word rows
+		out[e] = __funnelshift_r(row[k], row[k + 1], b);
+		out[stride + e] = d.w + a * r + (b + 1024u) % r;
+	}
+}
+
 // FormatError check (sievetable.hpp:67-79): bits >= r^2 of the last byte of
 // each table must be zero.
 __global__ void k_check_padding(const PrimeJob* __restrict__ jobs, uint32_t njobs,
@@ -323,6 +342,14 @@ cudaError_t launch_permute(const PrimeJob* d_jobs, uint32_t njobs, uint32_t max_
 	if (!njobs) return cudaSuccess;
 	const dim3 grid(grid_x(max_rr, kPermThreads, 256), njobs);
 	k_permute<<<grid, kPermThreads, 0, s>>>(d_jobs, d_row1, d_inv, d_packed);
+	return cudaGetLastError();
+}
+
+cudaError_t launch_wintab(const uint4* d_probes, uint32_t nprobes, uint32_t entries, const uint32_t* d_ext,
+                          uint32_t stride, uint32_t* d_out, cudaStream_t s)
+{
+	if (!entries) return cudaSuccess;
+	k_wintab<<<(entries + 255) / 256, 256, 0, s>>>(d_probes, nprobes, entries, d_ext, stride, d_out);
 	return cudaGetLastError();
 }
 
