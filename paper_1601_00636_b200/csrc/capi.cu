@@ -342,7 +342,7 @@ int finalize_set(cgpu_ctx* c, bool check_padding = false)
 	// register probes: the leading killable primes <= 31 (two-word rows), then,
 	// when all of 11..31 are among them, up to kMaxReg3 primes in (31, 63]
 	c->nreg = c->nreg2 = c->nreg3 = 0;
-	uint32_t cap2 = kMaxReg2, cap3 = 1;  // measured: one 3-word probe (r = 37) is best
+	uint32_t cap2 = kMaxReg2, cap3 = kStdReg3;
 	if (const char* e = std::getenv("CUBOID_MAX_REG_PROBES")) cap2 = std::min<uint32_t>(cap2, std::atoi(e));
 	if (const char* e = std::getenv("CUBOID_REG3_PROBES")) cap3 = std::min<uint32_t>(kMaxReg3, std::atoi(e));
 	auto add_reg = [&](uint32_t j) {
@@ -358,7 +358,13 @@ int finalize_set(cgpu_ctx* c, bool check_padding = false)
 		++c->nreg2;
 	}
 	const bool all_small = c->nreg2 == 7 && c->probe_r[0] == 11 && c->probe_r[6] == 31;
-	while (all_small && c->nreg < c->np && c->nreg3 < cap3 && c->probe_r[c->nreg] <= 63) {
+	auto tab_fits = [&](uint32_t extra) {  // window tables of the table probes within kTabStrideGen
+		uint32_t e = extra;
+		for (uint32_t j = 0; j < c->nreg && j < static_cast<uint32_t>(kTabProbes); ++j) e += c->reg_r[j] * c->reg_r[j];
+		return e <= kTabStrideGen;
+	};
+	while (all_small && c->nreg < c->np && c->nreg3 < cap3 && c->probe_r[c->nreg] <= 63 &&
+	       (c->nreg >= static_cast<uint32_t>(kTabProbes) || tab_fits(c->probe_r[c->nreg] * c->probe_r[c->nreg]))) {
 		add_reg(c->nreg);
 		++c->nreg3;
 	}
@@ -395,9 +401,9 @@ int finalize_set(cgpu_ctx* c, bool check_padding = false)
 		}
 	}
 	{
-		static const uint32_t std_primes[8] = {11, 13, 17, 19, 23, 29, 31, 37};
-		c->std_primes = c->nreg2 == 7 && c->nreg3 == 1 && !std::getenv("CUBOID_NO_STD_PRIMES");
-		for (uint32_t j = 0; c->std_primes && j < 8; ++j) c->std_primes = c->reg_r[j] == std_primes[j];
+		c->std_primes = c->nreg2 == 7 && c->nreg3 == static_cast<uint32_t>(kStdReg3) &&
+		                !std::getenv("CUBOID_NO_STD_PRIMES");
+		for (uint32_t j = 0; c->std_primes && j < c->nreg; ++j) c->std_primes = c->reg_r[j] == std_prime(j);
 	}
 	const size_t smem =
 	    sieve_smem_bytes(c->np, c->wtab_n ? (c->std_primes ? kTabStrideStd : kTabStrideGen) : 0);

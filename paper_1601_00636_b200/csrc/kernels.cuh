@@ -74,11 +74,25 @@ constexpr int kMaxFactors = 9;  // distinct prime factors of p < 2^32
 #define CGPU_TAB_PROBES 8
 #endif
 constexpr int kTabProbes = CGPU_TAB_PROBES;  // leading register probes read from a window table
+#ifndef CGPU_STD_REG3
+#define CGPU_STD_REG3 1
+#endif
+constexpr int kStdReg3 = CGPU_STD_REG3;  // 3-word register probes of the standard sets (measured best: 1)
+__host__ __device__ constexpr uint32_t std_prime(int j)
+{
+	return j == 0 ? 11 : j == 1 ? 13 : j == 2 ? 17 : j == 3 ? 19 : j == 4 ? 23 : j == 5 ? 29 : j == 6 ? 31
+	     : j == 7 ? 37 : j == 8 ? 41 : j == 9 ? 43 : 47;
+}
+__host__ __device__ constexpr uint32_t std_tab_entries(int j)
+{
+	return j <= 0 ? 0 : std_tab_entries(j - 1) + std_prime(j - 1) * std_prime(j - 1);
+}
 // Window tables of the table probes, all rows: sum over them of r^2 entries.
-// The 8 standard primes 11..37 need 4640; any admissible 8 table probes fit
-// 7424 (11..31 and one prime below 64: 3271 + 61^2 = 6992).
-constexpr uint32_t kTabStrideStd = 4640;
-constexpr uint32_t kTabStrideGen = 7424;
+// Standard sets: 11..37 need 4640. Other sets are admitted up to
+// kTabStrideGen (the host stops adding 3-word probes at that bound); any
+// 8 table probes fit (11..31 and one prime below 64: 3271 + 61^2 = 6992).
+constexpr uint32_t kTabStrideStd = std_tab_entries(7 + kStdReg3 < kTabProbes ? 7 + kStdReg3 : kTabProbes);
+constexpr uint32_t kTabStrideGen = kTabStrideStd > 7424 ? kTabStrideStd : 7424;
 constexpr int kQueue = 64;      // per-warp deep-probe work queue entries
 constexpr uint32_t kPlanChunk = 1024;  // row slots per plan CTA
 constexpr uint32_t kFacWords = 1 + kMaxFactors;  // per row slot: nf | even << 8, odd factors

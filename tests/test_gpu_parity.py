@@ -205,6 +205,46 @@ def test_random_ranges_vs_oracle(dev, seed):
             assert got == want
 
 
+REG_LAYOUTS = [
+    # (prime set, CUBOID_REG3_PROBES, CUBOID_NO_STD_PRIMES): every register /
+    # window-table probe layout the context can choose (capi.cu finalize_set)
+    (odd_primes(96), None, None),                                    # standard 11..37 (immediates)
+    (odd_primes(96), None, "1"),                                     # same primes, generic kernel
+    (odd_primes(96), "0", None),                                     # no 3-word probe
+    (odd_primes(96), "2", None),                                     # 37 table + 41 funnel probe
+    (odd_primes(96), "4", None),                                     # 37 table + 41, 43, 47 funnel
+    (primes_in_range(11, 31) + primes_in_range(61, 400), None, None),  # generic 3-word table r = 61
+    (primes_in_range(11, 31) + primes_in_range(59, 400), "3", None),   # 59 table + 61 funnel (67 > 63)
+    (primes_in_range(13, 400), None, None),                          # 11 absent: two-word probes only
+    ([11] + primes_in_range(37, 400), None, None),                   # one register probe
+    (primes_in_range(67, 500), None, None),                          # no register probes
+]
+
+
+@pytest.mark.parametrize("case", range(len(REG_LAYOUTS)))
+def test_register_probe_layouts_vs_oracle(dev, case, monkeypatch):
+    """Each register-probe layout (window-table probes, funnel probes, the
+    standard-prime instantiation, no register probes) against the oracle."""
+    P, reg3, nostd = REG_LAYOUTS[case]
+    for k, v in (("CUBOID_REG3_PROBES", reg3), ("CUBOID_NO_STD_PRIMES", nostd)):
+        if v is None:
+            monkeypatch.delenv(k, raising=False)
+        else:
+            monkeypatch.setenv(k, v)
+    tb, offs = port.build_set(P)
+    dev.load(P, tb)
+    rng = random.Random(100 + case)
+    for mode, lo, hi in ((N.TRIANGLE, 1, 1200), (N.TRIANGLE, rng.randrange(2000, 6000), None),
+                         (N.REGION, rng.randrange(152, 3000), None)):
+        hi = hi or lo + (60 if mode == N.TRIANGLE else 3)
+        o = port.sieve(tb, P, offs, lo, hi, mode)
+        r = dev.sieve(lo, hi, mode, surv_cap=1 << 22)
+        assert r.pairs_tested == o["pairs_tested"], (case, mode, lo, hi)
+        assert r.survivors == o["survivors"]
+        assert r.hist.tolist() == o["hist"].tolist()
+        assert np.array_equal(r.survivor_pairs, o["survivor_pairs"])
+
+
 def test_heavy_survivor_compaction(dev):
     """Weak sieve {11} (test_engine.cpp:177-197) over C1's triangle: 405,546
     survivors, emitted in canonical ascending (p, q) order."""
