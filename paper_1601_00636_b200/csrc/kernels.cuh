@@ -56,15 +56,19 @@ constexpr uint32_t kDeriveThreads = 256;
 
 // ---- K2: sieve ---------------------------------------------------------------
 
+// One 24-warp CTA per SM (80 registers x 768 threads). Measured against
+// three 8-warp CTAs per SM: the warp schedulers favour the SM's oldest CTA,
+// so with a static split the younger CTAs' warps finish last and the SM
+// runs its tail at a third of its warps (C5: 3.34 -> 3.04 ms).
 #ifndef CGPU_SIEVE_THREADS
-#define CGPU_SIEVE_THREADS 256
+#define CGPU_SIEVE_THREADS 768
 #endif
 constexpr int kSieveThreads = CGPU_SIEVE_THREADS;
 #ifndef CGPU_SIEVE_MIN_BLOCKS
-#define CGPU_SIEVE_MIN_BLOCKS 3
+#define CGPU_SIEVE_MIN_BLOCKS 1
 #endif
 constexpr int kSieveMinBlocks = CGPU_SIEVE_MIN_BLOCKS;  // CTAs per SM the register budget targets
-constexpr uint32_t kDefaultRowCost = 800;                 // window-equivalents per row setup
+constexpr uint32_t kDefaultRowCost = 500;                 // window-equivalents per row setup
 constexpr int kSieveWarps = kSieveThreads / 32;
 constexpr int kMaxReg2 = 8;     // leading probes held in registers with r <= 31 (2-word rows)
 constexpr int kMaxReg3 = 4;     // then with 31 < r <= 63 (3-word rows), after all of 11..31

@@ -528,6 +528,10 @@ __device__ __forceinline__ uint32_t dispatch_row(const SieveArgs& a, const WarpS
 	}
 }
 
+#ifdef CGPU_WARP_CLOCKS
+__device__ unsigned long long g_wclk[3 * 8192];
+#endif
+
 template <int NR2, int NR3, bool STD>
 __global__ void __launch_bounds__(kSieveThreads, kSieveMinBlocks) k_sieve(const SieveArgs a)
 {
@@ -557,6 +561,10 @@ __global__ void __launch_bounds__(kSieveThreads, kSieveMinBlocks) k_sieve(const 
 	__syncthreads();
 
 	CGPU_CHECK(sieve_smem_bytes(a.np, a.wtab_n ? TS : 0) <= dynamic_smem_size());
+#ifdef CGPU_WARP_CLOCKS
+	unsigned long long t_start;
+	asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+#endif
 	const uint32_t n_chunks = plan_chunks(a.n_slots);
 	const unsigned long long W = a.chunk_off[n_chunks];
 	const unsigned long long nwarps = static_cast<unsigned long long>(gridDim.x) * kSieveWarps;
@@ -640,6 +648,20 @@ __global__ void __launch_bounds__(kSieveThreads, kSieveMinBlocks) k_sieve(const 
 		__syncwarp();
 	}
 
+#ifdef CGPU_WARP_CLOCKS
+	{  // experiment hook (tools/warp_clocks.py): per-warp {start, end, smid}
+		unsigned long long t_end;
+		asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+		uint32_t smid;
+		asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+		const uint32_t gwi = blockIdx.x * kSieveWarps + wib;
+		if (lane == 0 && gwi < 8192) {
+			g_wclk[3 * gwi] = t_start;
+			g_wclk[3 * gwi + 1] = t_end;
+			g_wclk[3 * gwi + 2] = smid;
+		}
+	}
+#endif
 	// ---- CTA flush: per-warp counters -> global histogram ----
 	__syncthreads();
 	for (uint32_t j = threadIdx.x; j < a.np; j += blockDim.x) {
@@ -744,8 +766,15 @@ int sieve_grid(int device, int nr2, int nr3, bool std_primes, size_t smem)
 	int sms = 0, per_sm = 0;
 	cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
 	const void* fn = sieve_kernel_ptr(nr2, nr3, std_primes);
-	if (smem > 48 * 1024)
-		cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+	// Opt in to the device's full per-block shared memory once for every
+	// variant: contexts with different probe sets share the kernel, so a
+	// per-launch-size attribute set for one would reject another's launch.
+	int optin = 0;
+	cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+	cudaFuncAttributes fa{};
+	cudaFuncGetAttributes(&fa, fn);
+	cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+	                     optin - static_cast<int>(fa.sharedSizeBytes));
 	cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kSieveThreads, smem);
 	if (per_sm < 1) per_sm = 1;
 	return sms * per_sm;
@@ -784,5 +813,16 @@ cudaError_t launch_classify(const uint64_t* d_pq, uint64_t n, const uint8_t* d_p
 	k_classify<<<grid, 256, 0, s>>>(d_pq, n, d_packed, d_primes, d_offsets, nprimes, d_out);
 	return cudaGetLastError();
 }
+
+#ifdef CGPU_WARP_CLOCKS
+// experiment hook: per-warp {start, end, smid} of the last k_sieve launch
+extern "C" int cgpu_debug_warp_clocks(unsigned long long* out, unsigned n)
+{
+	return cudaMemcpyFromSymbol(out, g_wclk, sizeof(unsigned long long) * 3 * (n < 8192 ? n : 8192)) ==
+	               cudaSuccess
+	           ? 0
+	           : -1;
+}
+#endif
 
 }  // namespace cgpu
