@@ -725,10 +725,6 @@ int enqueue_sieve(cgpu_ctx* c, uint64_t p_lo, uint64_t q_start, uint64_t p_hi, u
 	const uint64_t blk_lo = p_lo / 100;
 	const uint64_t nblocks = launch_blocks(p_lo, p_hi);
 	CK(cudaEventRecord(c->ev[0], c->stream));
-	CK(cudaMemsetAsync(d_hist, 0, 8ull * c->primes.size(), c->stream));
-	CK(cudaMemsetAsync(d_counts, 0, 16, c->stream));
-	CK(launch_init_blocks(d_block_rmax, nblocks, blk_lo, G, g, c->stream));
-	if (nblocks) ++c->launches;
 	bool ev1 = false;
 
 	SieveArgs a{};
@@ -759,6 +755,7 @@ int enqueue_sieve(cgpu_ctx* c, uint64_t p_lo, uint64_t q_start, uint64_t p_hi, u
 	a.q_end = q_end;
 	a.mode = mode;
 	a.G = G;
+	a.g = g;
 	a.hist = d_hist;
 	a.nprimes = static_cast<uint32_t>(c->primes.size());
 	a.probe_rank = c->d_probe_rank.p;
@@ -768,18 +765,25 @@ int enqueue_sieve(cgpu_ctx* c, uint64_t p_lo, uint64_t q_start, uint64_t p_hi, u
 	a.surv = d_surv;
 	a.surv_cap = surv_cap;
 
-	if (!empty) {  // np == 0 (no table can kill): every candidate survives
-		// owned blocks: b in [blk_lo, blk_hi] with b % G == g
-		const uint64_t blk_hi = p_hi / 100;
-		const uint64_t first = blk_lo + ((g + G - blk_lo % G) % G);
-		const uint64_t owned = first <= blk_hi ? (blk_hi - first) / G + 1 : 0;
+	// owned blocks: b in [blk_lo, blk_hi] with b % G == g
+	const uint64_t blk_hi = p_hi / 100;
+	const uint64_t first = blk_lo + ((g + G - blk_lo % G) % G);
+	const uint64_t owned = !empty && first <= blk_hi ? (blk_hi - first) / G + 1 : 0;
+	if (!owned) {  // nothing to sieve: the outputs are still initialised
+		CK(cudaMemsetAsync(d_hist, 0, 8ull * c->primes.size(), c->stream));
+		CK(cudaMemsetAsync(d_counts, 0, 16, c->stream));
+		CK(launch_init_blocks(d_block_rmax, nblocks, blk_lo, G, g, c->stream));
+		if (nblocks) ++c->launches;
+	} else {  // np == 0 (no table can kill): every candidate survives
 		const size_t max_slots = static_cast<size_t>(std::min<uint64_t>(owned, kBlocksPerLaunch)) * 100;
 		CK(c->prefix.ensure(max_slots + 1));
 		CK(c->chunk_off.ensure(plan_chunks(static_cast<uint32_t>(max_slots)) + 1));
-		CK(c->tickets.ensure(2));
+		if (!c->tickets.p) {  // zeroed once: each kernel's last CTA resets its ticket
+			CK(c->tickets.ensure(2));
+			CK(cudaMemsetAsync(c->tickets.p, 0, 8, c->stream));
+		}
 		CK(c->rowfac.ensure(max_slots * kFacWords));
 		a.rowfac = c->rowfac.p;
-		CK(cudaMemsetAsync(c->tickets.p, 0, 8, c->stream));
 		a.prefix = c->prefix.p;
 		a.chunk_off = c->chunk_off.p;
 		a.tickets = c->tickets.p;
@@ -787,6 +791,7 @@ int enqueue_sieve(cgpu_ctx* c, uint64_t p_lo, uint64_t q_start, uint64_t p_hi, u
 			const uint64_t nb = std::min<uint64_t>(kBlocksPerLaunch, owned - ob);
 			a.blk0 = first + ob * G;
 			a.n_slots = static_cast<uint32_t>(nb * 100);
+			a.init = ob == 0;
 			CK(launch_plan(a, c->stream));
 			if (!ev1) CK(cudaEventRecord(c->ev[1], c->stream));  // sieve time excludes the first plan
 			ev1 = true;

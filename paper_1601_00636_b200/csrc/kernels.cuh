@@ -128,6 +128,8 @@ struct SieveArgs {
 	// work units before slot s = prefix[s] + chunk_off[s / kPlanChunk]
 	unsigned long long* prefix;        // [n_slots + 1] (chunk-local exclusive scan)
 	unsigned long long* chunk_off;     // [n_chunks + 1] (exclusive scan of chunk totals)
+	uint32_t g;                   // shard index (block b is owned when b % G == g)
+	uint32_t init;                // k_plan: zero hist/counters and initialise block_rmax first
 	uint32_t* tickets;                 // [2] last-CTA tickets (plan, sieve), zeroed per launch
 	uint32_t* rowfac;                  // [n_slots][kFacWords] row factorisations (k_plan)
 	// outputs

@@ -160,35 +160,72 @@ __device__ __forceinline__ unsigned long long block_excl_scan(unsigned long long
 	return x - v + (wid ? s_warp[wid - 1] : 0);
 }
 
-// Distinct prime factors of row p for the sieve's coprimality masks (trial
-// division by the primes below 2^16 with Barrett remainders): out[0] =
-// nf | even << 8, out[1..nf] = the odd prime factors that can divide some q of
-// the row (<= qhi). Empty rows get nf = 0.
-__device__ __forceinline__ void factorise(const SieveArgs& a, const RowBounds& rb, uint32_t* out)
+// Distinct prime factors of the CTA's rows for the sieve's coprimality masks,
+// by a segmented sieve in shared memory instead of per-row trial division
+// (which left every warp waiting on its slowest, prime, row: ~100 dependent
+// Barrett steps). Slots come in runs of 100 consecutive rows (one p/100
+// block each); one thread per (prime f <= sqrt(p_max), run) marks the
+// multiples of f, then each row divides its marked primes out and what is
+// left of p is 1 or its single prime factor above sqrt(p). Output per slot:
+// out[0] = nf | even << 8, out[1..nf] = the odd prime factors that can divide
+// some q of the row (<= qhi), ascending. Empty rows get nf = 0.
+struct PlanSmem {
+	uint32_t nf[kPlanChunk];
+	uint16_t fi[kPlanChunk][kMaxFactors];  // indices into a.fprimes
+};
+
+__device__ __forceinline__ void factorise_chunk(const SieveArgs& a, PlanSmem& sm, uint32_t c0, const RowBounds& rb,
+                                                uint32_t* out)
 {
-	uint32_t nf = 0, even = 0;
-	if (rb.qhi >= rb.qlo) {
-		const uint32_t p = static_cast<uint32_t>(rb.p);
-		const uint64_t qhi = rb.qhi;
-		uint32_t cof = p;
-		for (uint32_t i = 0; i < a.n_fprimes; ++i) {
-			const uint2 fp = __ldg(a.fprimes + i);
-			if (static_cast<uint64_t>(fp.x) * fp.x > cof) break;
-			uint32_t qt = __umulhi(cof, fp.y), rem = cof - qt * fp.x;
-			if (rem >= fp.x) { rem -= fp.x; ++qt; }
-			if (rem) continue;
-			if (fp.x == 2) even = 1;
-			else if (fp.x <= qhi && nf < kMaxFactors) out[1 + nf++] = fp.x;
-			do {  // divide f out of the cofactor
-				cof = qt;
-				qt = __umulhi(cof, fp.y);
-				rem = cof - qt * fp.x;
-				if (rem >= fp.x) { rem -= fp.x; ++qt; }
-			} while (!rem);
+	const uint32_t t = threadIdx.x;
+	sm.nf[t] = 0;
+	// largest row of the chunk (slots ascend in p)
+	const uint32_t s_last = min(c0 + kPlanChunk, a.n_slots) - 1;
+	const uint64_t p_last = (a.blk0 + static_cast<uint64_t>(s_last / 100) * a.G) * 100 + s_last % 100;
+	__syncthreads();
+	const uint32_t run0 = c0 / 100, nrun = s_last / 100 - run0 + 1;
+	for (uint32_t w = t;; w += kPlanChunk) {
+		const uint32_t i = w / nrun, k = run0 + w % nrun;
+		if (i >= a.n_fprimes) break;
+		const uint2 fp = __ldg(a.fprimes + i);
+		if (static_cast<uint64_t>(fp.x) * fp.x > p_last) break;  // i ascends with w
+		const uint32_t sa = max(c0, 100 * k), sb = min(s_last + 1, 100 * k + 100);  // slots of run k
+		const uint64_t P = (a.blk0 + static_cast<uint64_t>(k) * a.G) * 100;        // row of slot 100k
+		const uint32_t pa = static_cast<uint32_t>(P + (sa - 100 * k));              // p < 2^32
+		uint32_t rem = pa - __umulhi(pa, fp.y) * fp.x;
+		if (rem >= fp.x) rem -= fp.x;
+		for (uint32_t sl = sa + (rem ? fp.x - rem : 0); sl < sb; sl += fp.x) {
+			const uint32_t j = atomicAdd(&sm.nf[sl - c0], 1u);
+			if (j < kMaxFactors) sm.fi[sl - c0][j] = static_cast<uint16_t>(i);
 		}
-		if (cof > 1) {  // the prime factor above sqrt of the remaining cofactor
+	}
+	__syncthreads();
+	if (c0 + t >= a.n_slots) return;
+	uint32_t nf = 0, even = 0;
+	if (rb.qhi >= rb.qlo && rb.p > 1) {
+		const uint32_t n = min(sm.nf[t], static_cast<uint32_t>(kMaxFactors));
+		uint16_t f[kMaxFactors];
+		for (uint32_t j = 0; j < n; ++j) {  // ascending (insertion sort, n <= 9)
+			uint16_t v = sm.fi[t][j];
+			uint32_t k = j;
+			for (; k > 0 && f[k - 1] > v; --k) f[k] = f[k - 1];
+			f[k] = v;
+		}
+		uint32_t cof = static_cast<uint32_t>(rb.p);
+		for (uint32_t j = 0; j < n; ++j) {
+			const uint2 fp = __ldg(a.fprimes + f[j]);
+			for (;;) {  // divide f out of the cofactor
+				uint32_t qt = __umulhi(cof, fp.y), r = cof - qt * fp.x;
+				if (r >= fp.x) { r -= fp.x; ++qt; }
+				if (r) break;
+				cof = qt;
+			}
+			if (fp.x == 2) even = 1;
+			else if (fp.x <= rb.qhi && nf < kMaxFactors) out[1 + nf++] = fp.x;
+		}
+		if (cof > 1) {  // the prime factor above sqrt(p)
 			if (cof == 2) even = 1;
-			else if (cof <= qhi && nf < kMaxFactors) out[1 + nf++] = cof;
+			else if (cof <= rb.qhi && nf < kMaxFactors) out[1 + nf++] = cof;
 		}
 	}
 	out[0] = nf | (even << 8);
@@ -200,11 +237,18 @@ __global__ void __launch_bounds__(kPlanChunk) k_plan(const SieveArgs a)
 {
 	__shared__ unsigned long long s_warp[32];
 	__shared__ bool s_last;
+	__shared__ PlanSmem s_fac;
 	const uint32_t n = a.n_slots;
 	const uint32_t s = blockIdx.x * kPlanChunk + threadIdx.x;
+	if (a.init) {  // first plan of a scan: the sieve's outputs start from zero / owned blocks at 1
+		const uint64_t nt = static_cast<uint64_t>(gridDim.x) * kPlanChunk;
+		for (uint64_t i = s; i < a.n_blocks; i += nt) a.block_rmax[i] = ((a.blk_lo + i) % a.G == a.g) ? 1u : 0u;
+		for (uint64_t i = s; i < a.nprimes; i += nt) a.hist[i] = 0;
+		if (s < 2) a.counters[s] = 0;
+	}
 	const RowBounds rb = s < n ? slot_row(a, s) : RowBounds{0, 1, 0};
 	const unsigned long long u = s < n ? row_units(a, rb) : 0;
-	if (s < n) factorise(a, rb, a.rowfac + static_cast<size_t>(s) * kFacWords);
+	factorise_chunk(a, s_fac, blockIdx.x * kPlanChunk, rb, a.rowfac + static_cast<size_t>(s) * kFacWords);
 	unsigned long long total;
 	const unsigned long long ex = block_excl_scan(u, s_warp, total);
 	if (s < n) a.prefix[s] = ex;
