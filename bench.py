@@ -482,7 +482,8 @@ def run_ours(args, wl, primes):
             x = json.load(open(prof)).get("k_sieve", {}).get(wl["desc"][:2], {})
             ncu = {k: x.get(k) for k in ("round", "duration_ms", "issue_active_pct", "alu_pipe_pct",
                                           "xu_pipe_pct", "lsu_pipe_pct", "l1tex_throughput_pct",
-                                          "fma_pipe_pct", "warps_active_pct", "registers")}
+                                          "smem_wavefront_pct", "fma_pipe_pct", "warps_active_pct",
+                                          "registers")}
             if x.get("duration_ms"):
                 ncu["dram_gbs"] = x.get("dram_bytes", 0) / (x["duration_ms"] * 1e-3) / 1e9
         except (ValueError, AttributeError):

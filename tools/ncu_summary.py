@@ -30,6 +30,7 @@ KEYS = {
     "lsu_pipe_pct": "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active",
     "l1tex_throughput_pct": "l1tex__throughput.avg.pct_of_peak_sustained_active",
     "smem_wavefronts": "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum",
+    "smem_wavefront_pct": "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
     "warp_inst": "smsp__inst_executed.sum",
     "warps_active_pct": "sm__warps_active.avg.pct_of_peak_sustained_active",
     "sm_cycles_active_avg": "sm__cycles_active.avg",
