@@ -15,14 +15,15 @@
 // consecutive q in one row p; a probe for prime r is ONE funnel shift of the
 // row-extended table (row p mod r, starting at bit q0 mod r), so one probe
 // answers 32 pairs. Warps own contiguous slices of the linearised
-// (row, window) space, balanced by k_plan, which also factorises every p;
-// coprimality is then one periodic bit pattern per odd prime factor (the
-// window loop is specialised on the factor count) plus a constant mask for
-// f = 2. The leading probe primes (11..31, and the first in (31, 63]) are
-// read from a per-warp window table in shared memory (each entry: the 32-q
-// mask at one offset of the row, and a pointer to the lane's next entry), so
-// a probe costs two LDS and no ALU work on offsets; they count their first
-// kills by telescoping popcounts. Windows still alive after them (a few percent) are
+// (row, window) space, balanced by k_plan, which also factorises every p
+// (segmented sieve); coprimality is then one periodic bit pattern per odd
+// prime factor (the window loop is specialised on the factor count) plus a
+// constant mask for f = 2. The leading probe primes (11..31, and the first in
+// (31, 63]) are read from window tables resident in the CTA's shared memory
+// for every row (each entry: the 32-q mask at one offset of one row, and a
+// pointer to the lane's next entry), so a probe costs two LDS and no ALU work
+// on offsets; they count their first kills by telescoping popcounts. One
+// 24-warp CTA per SM. Windows still alive after them (a few percent) are
 // pushed to a per-warp queue in shared memory and probed against the deep
 // tables 32 at a time, one per lane, so the rare deep probes run at full SIMD
 // width. Tables that never kill (all-zero, e.g. r = 3, 5, 7) are not probed --
