@@ -51,7 +51,7 @@ WORKLOADS = {
     "C3": dict(k=64, p_lo=2, p_hi=10000, pairs=30397485,
                desc="C3: TRIANGLE sieve p<=1e4, 1<=q<p coprime, 64 odd primes 3..313"),
 }
-GATHER_CAP = 4096  # survivors per rank gathered inside the step (C3..C5 have 0)
+GATHER_CAP = 1024  # survivors per rank gathered inside the step (C1..C5 have 0; overflow is counted)
 
 
 # ---- host-side workload constants ------------------------------------------------------
