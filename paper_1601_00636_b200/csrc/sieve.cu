@@ -506,8 +506,8 @@ __device__ __forceinline__ uint32_t row_loop(const SieveArgs& a, const WarpSmem&
 			}
 			if (j + 1 < NREG) S[j + 1] += __popc(alive);
 		}
-		const uint32_t m = __ballot_sync(kFull, alive != 0);
-		if (m) {
+		if (__any_sync(kFull, alive != 0)) {  // VOTE.ANY to a predicate: one test per window
+			const uint32_t m = __ballot_sync(kFull, alive != 0);
 			CGPU_CHECK(qn + __popc(m) <= kQueue);
 			if (alive) w.queue[qn + __popc(m & lt)] = make_uint2(q0, alive);
 			qn += __popc(m);
