@@ -172,6 +172,21 @@ int main()
 	CHECK(head.pairs_tested == whole.pairs_tested && head.kill_histogram == whole.kill_histogram &&
 	      head.block_r_max == whole.block_r_max && head.resume_p == whole.resume_p);
 
+	// a scan polled for stops runs as several device tiles (~2^37 pairs each):
+	// the same statistics as one launch
+	{
+		std::atomic<bool> never{false};
+		ScanOptions po;
+		po.hooks.stop = &never;
+		const ScanStats tiled = gpu::scan(gpu_default, {152, 3}, 200000, {}, po);
+		const ScanStats one = gpu::scan(gpu_default, {152, 3}, 200000);
+		CHECK(!tiled.stopped);
+		CHECK(gpu::detail::tile_end(152, 200000) < 200000);
+		CHECK(tiled.pairs_tested == one.pairs_tested && tiled.kill_histogram == one.kill_histogram &&
+		      tiled.block_r_max == one.block_r_max && tiled.resume_p == one.resume_p &&
+		      tiled.resume_q == one.resume_q && tiled.survivors == one.survivors);
+	}
+
 	// TRIANGLE (BASELINE config 1: 32 odd primes, 2 <= p <= 2000)
 	const std::vector<uint32_t> P32 = odd_primes(32);
 	const SieveSet s32 = SieveSet::build(P32);

@@ -23,11 +23,13 @@
 // starts halts exactly where the reference's does -- at the batch_pairs-th q
 // visited (engine.hpp:248-257), same resume point and statistics (the span
 // before it is sieved with cgpu_sieve_span). A flag raised while the scan
-// runs is polled between tiles of kStopTileRows rows; the resume point is then
-// the first pair of the next tile. Either way ScanStats::merge of the two
+// runs is polled between device tiles of about kStopTilePairs REGION pairs
+// (~20 ms each at the B200's rate, whatever the row length); the resume point
+// is then the first pair of the next tile. Either way ScanStats::merge of the two
 // halves equals the full scan (test_engine.cpp:134-175).
 
 #include <chrono>
+#include <cmath>
 #include <cstdint>
 #include <cstring>
 #include <map>
@@ -41,7 +43,19 @@
 
 namespace cuboid::gpu {
 
-inline constexpr uint64_t kStopTileRows = 1000;
+inline constexpr uint64_t kStopTilePairs = 1ull << 37;
+
+namespace detail {
+// Last row of a tile starting at row p: REGION rows hold ~59p pairs, so rows
+// p..hi hold ~59/2 (hi^2 - p^2); pick hi for about kStopTilePairs of them.
+inline uint64_t tile_end(uint64_t p, uint64_t p_end)
+{
+	const long double x = static_cast<long double>(p) * p + 2.0L * kStopTilePairs / 59.0L;
+	uint64_t hi = static_cast<uint64_t>(std::sqrt(x));
+	if (hi < p) hi = p;
+	return hi < p_end ? hi : p_end;
+}
+}  // namespace detail
 
 struct Error : std::runtime_error {
 	int code;
@@ -289,13 +303,12 @@ inline ScanStats scan(const SieveSet& set, SearchPair start, uint64_t p_end, con
 		return st;
 	}
 	uint64_t p = start.p, q = start.q;
-	const uint64_t tile = opt.hooks.stop ? kStopTileRows : UINT64_MAX;
 	while (p <= p_end) {
 		if (opt.hooks.stop && opt.hooks.stop->load(std::memory_order_relaxed)) {
 			st.stopped = true;
 			break;
 		}
-		const uint64_t hi = (p_end - p >= tile) ? p + tile - 1 : p_end;
+		const uint64_t hi = opt.hooks.stop ? detail::tile_end(p, p_end) : p_end;
 		const detail::DeviceScan d = detail::run(c, set, p, q, hi, CGPU_REGION);
 		detail::fold(set, d, st, sink);
 		cuboid::detail::next_pair(hi, q_bounds(hi).q_high, q_bounds(hi).q_high, st.resume_p, st.resume_q);
