@@ -524,9 +524,7 @@ __device__ __forceinline__ uint32_t row_loop(const SieveArgs& a, const WarpSmem&
 	const uint32_t E = min(rc.w1, rc.wlast);  // windows below E are whole and in the slice
 	const uint32_t n_full = E > rc.w0 ? min((E - rc.w0) / 32, n_iter) : 0;
 	uint32_t it = 0;
-#ifndef CGPU_NO_EDGE_SPEC
 	for (; it < n_full; ++it) step(it, cuda::std::false_type{});
-#endif
 	for (; it < n_iter; ++it) step(it, cuda::std::true_type{});
 	if (qn) {
 		__syncwarp();
