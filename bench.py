@@ -218,6 +218,7 @@ def run_ours(args, wl, primes):
 
     from paper_1601_00636_b200 import _native as N
     from paper_1601_00636_b200.device import Device
+    from paper_1601_00636_b200 import parallel
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -261,6 +262,9 @@ def run_ours(args, wl, primes):
     N.check(L.cgpu_int32_peak(local, peaks))
     int_peak = {"alu_lop3": peaks[0], "fma_imad": peaks[1], "imad_lop3_3reg": peaks[2],
                 "imad_lop3_imm": peaks[3], "best": max(peaks)}
+    fpk = (C.c_double * 2)()
+    N.check(L.cgpu_fp32_peak(local, fpk))
+    fp_peak = {"ffma2_lane_fmas": fpk[0], "cube_mix_evals": fpk[1]}
 
     # ---- table build (BASELINE config 2): exhaustive Z_r^3, 256 primes --------------
     from paper_1601_00636_b200.primes import odd_primes
@@ -282,17 +286,22 @@ def run_ours(args, wl, primes):
         "config": "C2: first 256 odd primes (3..1621), every (a,b,t) in Z_r^3, sum r^3 = "
                   f"{tb_evals} evals, 25,869,968 B of tables",
         "ms": cube_ms, "production_build_ms": float(np.mean(prod_t)),
-        # k_cube evaluates Q as c0 + c1 s + ... + c4 s^4 (+ s^5) with the powers
-        # of s = t^2 tabulated per t: 4 IMAD multiply-accumulates + 1 IMAD for
-        # the divisibility-by-inverse test per eval, all on the FMA pipe (one
-        # ALU min beside them), so the bound is the measured IMAD-chain
-        # throughput / 5 per eval.
-        "roofline": {"bound": "int32_fma_pipe", "imad_per_eval": 5,
-                     "achieved": 5 * tb_evals / (cube_ms * 1e-3),
-                     "peak": int_peak["fma_imad"], "unit": "IMAD ops/s",
-                     "frac": 5 * tb_evals / (cube_ms * 1e-3) / int_peak["fma_imad"],
+        # k_cube_f2 evaluates A = c0 + c1 s + ... + c4 s^4 exactly in FP32 (balanced
+        # residues, |A| < 2^22, on top of 1.5 * 2^23) with two (a,b) pairs per
+        # FFMA2, then tests (A + s^5) for divisibility by r with one IMAD by
+        # r^-1 mod 2^32 and an unsigned min: 2 FFMA2 + 1 IMAD + 1 min per eval.
+        # The bound is that mix's measured throughput (cgpu_fp32_peak).
+        "roofline": {"bound": "fp32_fma_pipes", "instr_per_eval": "2 FFMA2 + 1 IMAD + 1 VIMNMX",
+                     "achieved": tb_evals / (cube_ms * 1e-3),
+                     "peak": fp_peak["cube_mix_evals"], "unit": "evals/s",
+                     "frac": tb_evals / (cube_ms * 1e-3) / fp_peak["cube_mix_evals"],
+                     "fp32_peaks": fp_peak,
+                     "imad_path_peak_evals": int_peak["fma_imad"] / 5,
                      "horner_ops_per_eval_survey": 27,
-                     "note": "SURVEY 8(d) counts 27 INT32 ops/eval for Horner; the kernel issues 7"},
+                     "note": "SURVEY 8(d) counts 27 INT32 ops/eval for Horner; the kernel issues 4 "
+                             "(+ shared loads and loop control amortised over 16 pairs per thread). "
+                             "imad_path_peak_evals = the ceiling of the previous all-IMAD kernel "
+                             "(5 IMAD/eval), still used for r = 2 and r > 2039"},
     }
 
     # ---- the paper's historical scan, for the published figure ------
@@ -416,10 +425,13 @@ def run_ours(args, wl, primes):
             self.done = torch.cuda.Event()
 
         def issue(self):
-            N.check(L.cgpu_tables_load(self.dev._ctx, pr.ctypes.data_as(C.c_void_p), n,
-                                       C.c_void_p(pinned.data_ptr()), len(tables)))
             b = self.buf
             with torch.cuda.stream(self.stream):
+                if world > 1:  # 1/G of the bytes per rank over PCIe, all-gathered over NVLink
+                    self.full = parallel.load_tables_sharded(self.dev, pr, pinned)
+                else:
+                    N.check(L.cgpu_tables_load(self.dev._ctx, pr.ctypes.data_as(C.c_void_p), n,
+                                               C.c_void_p(pinned.data_ptr()), len(tables)))
                 if world > 1:
                     b[n_acc + nblocks:].zero_()
                 N.check(L.cgpu_sieve_launch_dev(
@@ -513,12 +525,15 @@ def run_ours(args, wl, primes):
                                       "all-reduce(SUM) of counts/histogram/block r_max/survivor slices"},
             "parity": "ok" if parity_ok else "MISMATCH",
             "e2e": {"value": pairs * args.steps / e2e_total, "unit": "pairs/s",
-                    "h2d_bytes_per_step": len(tables) + 4 * n,
+                    "h2d_bytes_per_step": (parallel.table_slice(len(tables), world, 0)[2] if world > 1
+                                           else len(tables)) + 4 * n,
                     "d2h_bytes_per_step": 8 * buf.numel(),
                     "ms_per_step": 1e3 * e2e_total / args.steps,
                     "path": "per step: cgpu_tables_load(pinned host tables) + cgpu_sieve_launch_dev + "
                             "reduce + D2H of the result vector; two contexts/streams pipelined 2 deep "
-                            "(step i+1's upload overlaps step i's sieve)"},
+                            "(step i+1's upload overlaps step i's sieve); at N>1 each rank uploads "
+                            "1/N of the tables (h2d bytes are per rank) and one all-gather assembles "
+                            "the set (parallel.load_tables_sharded, cgpu_tables_load_dev)"},
             "gpu_launches": launches,
             "roofline": roof,
             "table_build": table_build,

@@ -97,6 +97,13 @@ int cgpu_tables_build(cgpu_ctx* ctx, const uint32_t* primes, uint32_t n, int alg
 int cgpu_tables_load(cgpu_ctx* ctx, const uint32_t* primes, uint32_t n, const uint8_t* bytes,
                      uint64_t nbytes);
 
+/* As cgpu_tables_load, from DEVICE memory on ctx's device (ordered on ctx's
+ * stream): the multi-GPU upload path, where each rank copies 1/G of the host
+ * tables over PCIe and the full set is all-gathered over NVLink first
+ * (parallel.py load_tables_sharded). */
+int cgpu_tables_load_dev(cgpu_ctx* ctx, const uint32_t* primes, uint32_t n, const void* d_bytes,
+                         uint64_t nbytes);
+
 /* Copies the resident packed tables back (total_bytes) -- byte-identical to
  * serialize_tables (sievetable.hpp:229). */
 int cgpu_tables_download(cgpu_ctx* ctx, uint8_t* out_bytes, uint64_t cap);
@@ -192,6 +199,12 @@ int cgpu_last_timings(cgpu_ctx* ctx, float* ms3);
  * interleaved (3 register sources each), ops4[3] = IMAD + LOP3 with
  * immediates (the issue-bound ceiling). The roofline denominators of the bench. */
 int cgpu_int32_peak(int device, double* ops4);
+
+/* Measured FP32-pipe throughput of `device`: ops2[0] = FFMA2 chains in lane
+ * FMAs/s (3 register sources), ops2[1] = the exhaustive table build's
+ * evaluation mix (2 FFMA2 + IMAD + min per evaluation, k_cube_f2) in
+ * evaluations/s -- the table build's roofline denominator. */
+int cgpu_fp32_peak(int device, double* ops2);
 
 /* Number of kernels the last cgpu_sieve_launch / cgpu_tables_* enqueued. */
 int cgpu_last_launch_count(cgpu_ctx* ctx, uint32_t* n);

@@ -34,6 +34,7 @@ SIGNATURES = {
     "cgpu_tables_build": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint32, C.c_int, C.c_void_p,
                                     C.c_void_p, _u64p]),
     "cgpu_tables_load": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint32, C.c_void_p, C.c_uint64]),
+    "cgpu_tables_load_dev": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint32, C.c_void_p, C.c_uint64]),
     "cgpu_tables_download": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64]),
     "cgpu_tables_info": (C.c_int, [C.c_void_p, _u32p, C.c_void_p]),
     "cgpu_build_tables": (C.c_int, [C.c_int, C.c_void_p, C.c_uint32, C.c_int, C.c_void_p,
@@ -57,6 +58,7 @@ SIGNATURES = {
                                   C.c_uint64]),
     "cgpu_last_timings": (C.c_int, [C.c_void_p, C.POINTER(C.c_float)]),
     "cgpu_int32_peak": (C.c_int, [C.c_int, C.POINTER(C.c_double)]),
+    "cgpu_fp32_peak": (C.c_int, [C.c_int, C.POINTER(C.c_double)]),
     "cgpu_last_launch_count": (C.c_int, [C.c_void_p, _u32p]),
     "cgpu_classify": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p]),
     "cgpu_q_bounds": (C.c_int, [C.c_uint64, _u64p, _u64p]),

@@ -465,8 +465,8 @@ int cgpu_tables_build(cgpu_ctx* c, const uint32_t* primes, uint32_t n, int algor
 		const uint32_t rmax = byr.front().r;
 		CK(cudaEventRecord(c->ev[0], c->stream));
 		if (algorithm == CGPU_BUILD_EXHAUSTIVE) {
-			CK(launch_cube(c->jobs_build.p, n, rmax * rmax, c->packed.p, c->stream));
-			c->launches += 1;
+			CK(launch_cube(c->jobs_build.p, byr.data(), n, c->packed.p, c->stream));
+			c->launches += cube_launches(byr.data(), n);
 			CK(cudaEventRecord(c->ev[1], c->stream));
 			for (auto r : c->primes) evals += static_cast<uint64_t>(r) * r * r;
 		} else {
@@ -502,8 +502,23 @@ int cgpu_tables_build(cgpu_ctx* c, const uint32_t* primes, uint32_t n, int algor
 	return CGPU_OK;
 }
 
+static int tables_load(cgpu_ctx* c, const uint32_t* primes, uint32_t n, const void* bytes, uint64_t nbytes,
+                       cudaMemcpyKind kind);
+
 int cgpu_tables_load(cgpu_ctx* c, const uint32_t* primes, uint32_t n, const uint8_t* bytes,
                      uint64_t nbytes)
+{
+	return tables_load(c, primes, n, bytes, nbytes, cudaMemcpyHostToDevice);
+}
+
+int cgpu_tables_load_dev(cgpu_ctx* c, const uint32_t* primes, uint32_t n, const void* d_bytes,
+                         uint64_t nbytes)
+{
+	return tables_load(c, primes, n, d_bytes, nbytes, cudaMemcpyDeviceToDevice);
+}
+
+static int tables_load(cgpu_ctx* c, const uint32_t* primes, uint32_t n, const void* bytes, uint64_t nbytes,
+                       cudaMemcpyKind kind)
 {
 	if (!c) return set_err(CGPU_ERR_INVALID, "null ctx");
 	CK(cudaSetDevice(c->device));
@@ -514,7 +529,7 @@ int cgpu_tables_load(cgpu_ctx* c, const uint32_t* primes, uint32_t n, const uint
 	c->launches = 0;
 	if (n) {
 		if (!bytes) return set_err(CGPU_ERR_INVALID, "null table bytes");
-		CK(cudaMemcpyAsync(c->packed.p, bytes, total, cudaMemcpyHostToDevice, c->stream));
+		CK(cudaMemcpyAsync(c->packed.p, bytes, total, kind, c->stream));
 		std::vector<uint32_t> eb;
 		uint64_t ew = 0;
 		std::vector<PrimeJob> jobs = make_jobs(c->primes, c->offsets, eb, ew);
@@ -938,6 +953,17 @@ int cgpu_int32_peak(int device, double* ops4)
 		return set_err(CGPU_ERR_NO_DEVICE, "no CUDA device visible: cuboid_gpu has no CPU fallback");
 	CK(cudaSetDevice(device));
 	CK(run_int_peak(device, ops4));
+	return CGPU_OK;
+}
+
+int cgpu_fp32_peak(int device, double* ops2)
+{
+	if (!ops2) return set_err(CGPU_ERR_INVALID, "null argument");
+	int count = 0;
+	if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0)
+		return set_err(CGPU_ERR_NO_DEVICE, "no CUDA device visible: cuboid_gpu has no CPU fallback");
+	CK(cudaSetDevice(device));
+	CK(run_fp_peak(device, ops2));
 	return CGPU_OK;
 }
 

@@ -19,9 +19,10 @@ struct PrimeJob {
 };
 
 // Exhaustive cube: all (a,b,t) in Z_r^3, no early exit. `jobs` sorted by
-// descending r (blockIdx.y = job); max_rr = largest r^2.
-cudaError_t launch_cube(const PrimeJob* d_jobs, uint32_t njobs, uint32_t max_rr,
+// descending r (blockIdx.y = job); h_jobs is the host copy of d_jobs.
+cudaError_t launch_cube(const PrimeJob* d_jobs, const PrimeJob* h_jobs, uint32_t njobs,
                         uint8_t* d_packed, cudaStream_t s);
+uint32_t cube_launches(const PrimeJob* h_jobs, uint32_t njobs);  // kernels launch_cube issues
 
 // Production: row 1 (t <= r/2, early exit) + modular inverses, then the
 // permuted, packed r x r table.
@@ -50,6 +51,8 @@ cudaError_t launch_check_padding(const PrimeJob* d_jobs, uint32_t njobs, const u
 
 constexpr uint32_t kCubeThreads = 256;
 constexpr int kCubePairs = 4;  // (a,b) pairs per thread in k_cube
+constexpr int kCubeF2Pairs = 16;  // (a,b) pairs per thread in k_cube_f2 (two per FFMA2)
+constexpr uint32_t kCubeF2MaxR = 2039;  // largest prime with h + 4h^2 < 2^22, h = (r-1)/2
 constexpr uint32_t kPermThreads = 256;
 constexpr uint32_t kRow1Threads = 128;
 constexpr uint32_t kDeriveThreads = 256;
@@ -160,5 +163,7 @@ cudaError_t launch_classify(const uint64_t* d_pq, uint64_t n, const uint8_t* d_p
 // INT32 pipe peaks (peak.cu), thread-ops/s: {LOP3-only, IMAD-only,
 // IMAD+LOP3 3-register, IMAD+LOP3 immediate forms}.
 cudaError_t run_int_peak(int device, double out[4]);
+// FP32 pipes (peak.cu): {FFMA2 lane-FMAs/s, k_cube_f2 evaluation-mix evals/s}.
+cudaError_t run_fp_peak(int device, double out[2]);
 
 }  // namespace cgpu

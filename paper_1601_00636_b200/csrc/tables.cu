@@ -155,6 +155,126 @@ __global__ void __launch_bounds__(kCubeThreads) k_cube(const PrimeJob* __restric
 	}
 }
 
+// Packed FP32 pair helpers (sm_100 FFMA2: two FMAs per lane per instruction;
+// a broadcast scalar operand costs nothing -- ptxas folds {b, b} into it).
+__device__ __forceinline__ unsigned long long f32x2(float x, float y)
+{
+	unsigned long long r;
+	asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(x), "f"(y));
+	return r;
+}
+
+__device__ __forceinline__ unsigned long long ffma2(unsigned long long a, float b, unsigned long long c)
+{
+	unsigned long long d;
+	asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(f32x2(b, b)), "l"(c));
+	return d;
+}
+
+// Balanced residue of x in [0, r): the representative in [-(r-1)/2, (r-1)/2].
+__device__ __forceinline__ float balanced(uint32_t x, uint32_t r)
+{
+	return static_cast<float>(x <= r / 2 ? static_cast<int>(x) : static_cast<int>(x) - static_cast<int>(r));
+}
+
+// Exhaustive cube on the FP32 pipes, for odd r <= kCubeF2MaxR. Same bit as
+// k_cube (and modpoly.hpp:116-125): Q_ab(t) = 0 mod r for some t.
+//
+// With the coefficients c_k and the powers s^k mod r in balanced form (|.| <=
+// h = (r-1)/2), A = c0 + c1 s + c2 s^2 + c3 s^3 + c4 s^4 is an integer with
+// |A| <= h + 4h^2 < 2^22 and so is every partial sum. Accumulated on top of
+// M = 1.5 * 2^23 every FMA result is an integer in (2^23, 2^24), where the
+// float grid is the integers: the four FMAs are exact, and the float's bit
+// pattern is 0x4B400000 + A. Two (a,b) pairs share one FFMA2 (the s^k operand
+// is broadcast). The root test is then the same divisibility-by-inverse as
+// k_cube on x = A + s^5 + K r >= 0 (K r >= 2^22), folded into one IMAD:
+//     x r^-1 = bits(v) r^-1 + w_t,   w_t = (s^5 + K r - 0x4B400000) r^-1,
+// all mod 2^32, and r | x iff x r^-1 mod 2^32 <= (2^32 - 1) / r.
+// Per evaluation: 2 FFMA2 (half of four) + 1 IMAD + 1 min, against k_cube's
+// 5 IMAD + 1 min on the IMAD-only half of the FMA pipes. PAIRS = 16 pairs per
+// thread amortise the shared-memory loads and loop control (measured on C2:
+// 4 -> 61 ms, 8 -> 60 ms, 16 -> 56 ms, at 128 registers, 2 CTAs per SM).
+template <int PAIRS>
+__global__ void __launch_bounds__(kCubeThreads) k_cube_f2(const PrimeJob* __restrict__ jobs,
+                                                          uint8_t* __restrict__ packed)
+{
+	extern __shared__ float4 s_b[];  // [r] balanced {s, s^2, s^3, s^4} then [r] w_t
+	const PrimeJob job = jobs[blockIdx.y];
+	const uint32_t r = job.r, m = job.m;
+	const uint32_t rr = r * r;
+	constexpr uint32_t per_cta = kCubeThreads * PAIRS;
+	if (blockIdx.x * per_cta >= rr) return;
+	uint32_t rinv = r;
+	for (int i = 0; i < 5; ++i) rinv *= 2u - r * rinv;
+	const uint32_t lim = 0xffffffffu / r;
+	const uint32_t Kr = ((1u << 22) + r - 1) / r * r;
+	uint32_t* s_w = reinterpret_cast<uint32_t*>(s_b + r);
+	for (uint32_t t = threadIdx.x; t < r; t += blockDim.x) {
+		const uint32_t s1 = mod_full(t * t, r, m);
+		const uint32_t s2 = mod_full(s1 * s1, r, m);
+		const uint32_t s3 = mod_full(s2 * s1, r, m);
+		const uint32_t s4 = mod_full(s3 * s1, r, m);
+		const uint32_t s5 = mod_full(s4 * s1, r, m);
+		s_b[t] = make_float4(balanced(s1, r), balanced(s2, r), balanced(s3, r), balanced(s4, r));
+		s_w[t] = (s5 + Kr - 0x4B400000u) * rinv;
+	}
+	__syncthreads();
+	const uint32_t tbytes = (rr + 7) >> 3;
+	const uint32_t lane = threadIdx.x & 31;
+	constexpr int NP = PAIRS / 2;  // FFMA2 pair slots
+	for (uint32_t base = blockIdx.x * per_cta; base < rr; base += gridDim.x * per_cta) {
+		unsigned long long C1[NP], C2[NP], C3[NP], C4[NP], V0[NP];
+		uint32_t mn[PAIRS];
+#pragma unroll
+		for (int j = 0; j < NP; ++j) {
+			float c[2][5];
+#pragma unroll
+			for (int h = 0; h < 2; ++h) {
+				const uint32_t i = base + (2 * j + h) * kCubeThreads + threadIdx.x;
+				uint32_t a = __umulhi(i, m), b = i - a * r;
+				if (b >= r) { b -= r; ++a; }
+				uint32_t cu[5];
+				mod_coeffs(i < rr ? a : 0, i < rr ? b : 0, r, m, cu);  // c4, c3, c2, c1, c0
+#pragma unroll
+				for (int k = 0; k < 5; ++k) c[h][k] = balanced(cu[k], r);
+				mn[2 * j + h] = 0xffffffffu;
+			}
+			C4[j] = f32x2(c[0][0], c[1][0]);
+			C3[j] = f32x2(c[0][1], c[1][1]);
+			C2[j] = f32x2(c[0][2], c[1][2]);
+			C1[j] = f32x2(c[0][3], c[1][3]);
+			V0[j] = f32x2(12582912.0f + c[0][4], 12582912.0f + c[1][4]);
+		}
+#pragma unroll 2
+		for (uint32_t t = 0; t < r; ++t) {
+			const float4 bp = s_b[t];
+			const uint32_t w = s_w[t];
+			// power-major: consecutive FFMA2 share the broadcast operand
+			// (register reuse) and the NP chains are independent
+			unsigned long long v[NP];
+#pragma unroll
+			for (int j = 0; j < NP; ++j) v[j] = ffma2(C4[j], bp.w, V0[j]);
+#pragma unroll
+			for (int j = 0; j < NP; ++j) v[j] = ffma2(C3[j], bp.z, v[j]);
+#pragma unroll
+			for (int j = 0; j < NP; ++j) v[j] = ffma2(C2[j], bp.y, v[j]);
+#pragma unroll
+			for (int j = 0; j < NP; ++j) v[j] = ffma2(C1[j], bp.x, v[j]);
+#pragma unroll
+			for (int j = 0; j < NP; ++j) {
+				mn[2 * j] = min(mn[2 * j], static_cast<uint32_t>(v[j]) * rinv + w);
+				mn[2 * j + 1] = min(mn[2 * j + 1], static_cast<uint32_t>(v[j] >> 32) * rinv + w);
+			}
+		}
+#pragma unroll
+		for (int k = 0; k < PAIRS; ++k) {
+			const uint32_t i = base + k * kCubeThreads + threadIdx.x;
+			const uint32_t word = __ballot_sync(kFull, i < rr && mn[k] > lim);
+			store_word_bytes(packed + job.byte_off, tbytes, i - lane, word, lane);
+		}
+	}
+}
+
 __device__ __forceinline__ uint32_t pow_mod(uint32_t a, uint32_t e, uint32_t r, uint32_t m)
 {
 	uint32_t x = 1 % r;
@@ -311,19 +431,44 @@ uint32_t grid_x(uint64_t units, uint32_t per_cta, uint32_t cap)
 
 }  // namespace
 
-// total_ctas = max over jobs of ceil(r^2/256), the x extent.
-cudaError_t launch_cube(const PrimeJob* d_jobs, uint32_t njobs, uint32_t max_rr, uint8_t* d_packed,
+// Jobs are sorted by descending r. Odd r <= kCubeF2MaxR (every BASELINE set)
+// run on the FP32 pipes (k_cube_f2); larger r and r = 2 (the last job when
+// present) on the IMAD path (k_cube). One launch per contiguous group.
+cudaError_t launch_cube(const PrimeJob* d_jobs, const PrimeJob* h_jobs, uint32_t njobs, uint8_t* d_packed,
                         cudaStream_t s)
 {
 	if (!njobs) return cudaSuccess;
-	const dim3 grid(grid_x(max_rr, kCubeThreads * kCubePairs, 8192), njobs);
-	uint32_t max_r = 1;
-	while (max_r * max_r < max_rr) ++max_r;
-	const size_t smem = (sizeof(uint4) + sizeof(uint32_t)) * max_r;  // 32 KB at r = 1621
-	if (smem > 48 * 1024)
-		cudaFuncSetAttribute(k_cube, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-	k_cube<<<grid, kCubeThreads, smem, s>>>(d_jobs, d_packed);
+	uint32_t nbig = 0;
+	while (nbig < njobs && h_jobs[nbig].r > kCubeF2MaxR) ++nbig;
+	const bool two = h_jobs[njobs - 1].r == 2;
+	const uint32_t f2_end = two ? njobs - 1 : njobs;
+	auto int_launch = [&](uint32_t j0, uint32_t n) {
+		const uint32_t r0 = h_jobs[j0].r;  // largest of the group
+		const dim3 grid(grid_x(static_cast<uint64_t>(r0) * r0, kCubeThreads * kCubePairs, 8192), n);
+		const size_t smem = (sizeof(uint4) + sizeof(uint32_t)) * r0;
+		if (smem > 48 * 1024)
+			cudaFuncSetAttribute(k_cube, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+		k_cube<<<grid, kCubeThreads, smem, s>>>(d_jobs + j0, d_packed);
+	};
+	if (nbig) int_launch(0, nbig);
+	if (f2_end > nbig) {
+		const uint32_t r0 = h_jobs[nbig].r;
+		const dim3 grid(grid_x(static_cast<uint64_t>(r0) * r0, kCubeThreads * kCubeF2Pairs, 8192), f2_end - nbig);
+		const size_t smem = (sizeof(float4) + sizeof(uint32_t)) * r0;  // 40 KB at r = 2039
+		k_cube_f2<kCubeF2Pairs><<<grid, kCubeThreads, smem, s>>>(d_jobs + nbig, d_packed);
+	}
+	if (two && njobs - 1 >= nbig) int_launch(njobs - 1, 1);
 	return cudaGetLastError();
+}
+
+uint32_t cube_launches(const PrimeJob* h_jobs, uint32_t njobs)
+{
+	if (!njobs) return 0;
+	uint32_t nbig = 0;
+	while (nbig < njobs && h_jobs[nbig].r > kCubeF2MaxR) ++nbig;
+	const bool two = h_jobs[njobs - 1].r == 2;
+	const uint32_t f2_end = two ? njobs - 1 : njobs;
+	return (nbig ? 1 : 0) + (f2_end > nbig ? 1 : 0) + (two && njobs - 1 >= nbig ? 1 : 0);
 }
 
 cudaError_t launch_row1(const PrimeJob* d_jobs, uint32_t njobs, uint32_t max_r, uint8_t* d_row1,

@@ -84,6 +84,14 @@ class Device:
         self.primes = pr.copy()
         self.offsets, self.total_bytes = self.layout(pr)
 
+    def load_dev(self, primes, d_ptr: int, nbytes: int):
+        """Upload packed tables that already sit in device memory on this GPU
+        (e.g. all-gathered by parallel.load_tables_sharded), on this stream."""
+        pr = np.ascontiguousarray(primes, dtype=np.uint32)
+        N.check(N.lib().cgpu_tables_load_dev(self._ctx, _ptr(pr), len(pr), C.c_void_p(d_ptr), int(nbytes)))
+        self.primes = pr.copy()
+        self.offsets, self.total_bytes = self.layout(pr)
+
     def save_files(self, tables_path: str, index_path: str):
         """save_sieve_files of the resident set (sievetable.hpp:334-339)."""
         N.check(N.lib().cgpu_tables_save_files(self._ctx, tables_path.encode(), index_path.encode()))

@@ -104,6 +104,58 @@ def gather_survivors(keys, count: int, group=None):
     return np.stack([allk >> np.uint64(32), allk & np.uint64(0xFFFFFFFF)], 1)
 
 
+def table_slice(total: int, G: int, g: int) -> tuple[int, int, int]:
+    """Rank g's share of a G-way table upload: (lo, hi, chunk) with equal
+    chunks of ceil(total / G) bytes (the last rank's slice may be short or
+    empty); the concatenation of all slices is the whole set."""
+    chunk = -(-total // G) if total else 0
+    lo = min(total, g * chunk)
+    return lo, min(total, lo + chunk), chunk
+
+
+def allgather_tables(host, device=None, group=None):
+    """Every rank's copy of the host table set `host` (uint8 tensor, pinned
+    for the NCCL path) with each rank moving only 1/G of it to its GPU: rank g
+    copies its slice (table_slice) and one all-gather assembles the whole set
+    -- over NVLink under NCCL, into a tensor on `device`, ordered on torch's
+    current stream. On gloo the slices and the result stay in host memory."""
+    import torch
+    import torch.distributed as dist
+    G = dist.get_world_size(group)
+    g = dist.get_rank(group)
+    total = host.numel()
+    lo, hi, chunk = table_slice(total, G, g)
+    nccl = dist.get_backend(group) == "nccl"
+    where = device if nccl else torch.device("cpu")
+    mine = torch.zeros(max(chunk, 1), dtype=torch.uint8, device=where)
+    mine[:hi - lo].copy_(host[lo:hi], non_blocking=nccl)
+    if nccl:
+        full = torch.empty(mine.numel() * G, dtype=torch.uint8, device=where)
+        dist.all_gather_into_tensor(full, mine, group=group)
+    else:
+        parts = [torch.empty_like(mine) for _ in range(G)]
+        dist.all_gather(parts, mine, group=group)
+        full = torch.cat(parts)
+    return full[:total]
+
+
+def load_tables_sharded(dev, primes, host, group=None):
+    """Make the host table set resident on every rank's GPU through
+    allgather_tables (1/G of the bytes over each rank's PCIe link), then load
+    it from device memory (cgpu_tables_load_dev: padding check, device
+    layouts) on torch's current stream, which must be the context's stream.
+    Returns the gathered tensor (keep it alive until the stream has run)."""
+    import torch
+    import torch.distributed as dist
+    pr = np.ascontiguousarray(primes, dtype=np.uint32)
+    full = allgather_tables(host, torch.device("cuda", dev.device), group)
+    if full.is_cuda:
+        dev.load_dev(pr, full.data_ptr(), full.numel())
+    else:
+        dev.load(pr, full.numpy().tobytes())
+    return full
+
+
 class ShardedSieve:
     """The product multi-GPU path: this rank's shard on its own GPU, results
     reduced over the default process group (NCCL)."""

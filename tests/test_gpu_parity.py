@@ -69,10 +69,21 @@ def test_single_tables_vs_oracle(dev):
     assert cuboid.build_table(11).bytes == bytes.fromhex("00E09F7EEDED76CF7BDEEDF6D62FFF00")
     for r in (2, 3, 5, 7):
         assert cuboid.build_table(r).bytes == bytes((r * r + 7) // 8)
-    for r in primes_in_range(2, 97) + [541, 1021, 4099, 9689]:
-        for alg in (N.BUILD_PRODUCTION, N.BUILD_EXHAUSTIVE) if r < 2000 else (N.BUILD_PRODUCTION,):
+    for r in primes_in_range(2, 97) + [541, 1021, 2039, 2053, 4099, 9689]:
+        for alg in (N.BUILD_PRODUCTION, N.BUILD_EXHAUSTIVE) if r < 2100 else (N.BUILD_PRODUCTION,):
             tb, _ = dev.build([r], alg)
             assert tb == port.build_table(r), (r, alg)
+
+
+def test_exhaustive_mixed_paths(dev):
+    """One exhaustive build whose primes take every k_cube path at once: r = 2
+    and r > 2039 on the IMAD kernel, odd r <= 2039 on the FFMA2 kernel (the
+    boundary primes 2039 and 2053 on either side)."""
+    P = [2, 3, 13, 1621, 2039, 2053]
+    tb, evals = dev.build(P, N.BUILD_EXHAUSTIVE)
+    assert evals == sum(r ** 3 for r in P)
+    want, _ = port.build_set(P)
+    assert tb == want
 
 
 @pytest.mark.parametrize("r", [0, 1, 4, 9697, 10007])

@@ -41,6 +41,40 @@ def test_partition_balances_triangle_work():
     assert max(work) / min(work) < 1.01
 
 
+def test_table_slices_cover_the_set_once():
+    for total in (0, 1, 7, 21873, 25869968):
+        for G in (1, 2, 3, 8):
+            got = []
+            for g in range(G):
+                lo, hi, chunk = parallel.table_slice(total, G, g)
+                assert 0 <= hi - lo <= chunk and (hi - lo == chunk or hi == total)
+                got.append((lo, hi))
+            assert got[0][0] == 0 and got[-1][1] == total
+            assert all(got[i][1] == got[i + 1][0] for i in range(G - 1))
+
+
+def _gather_worker(rank, world, port_, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port_)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    for k in (32, 64):
+        tb, _ = port.build_set(odd_primes(k))
+        host = torch.frombuffer(bytearray(tb), dtype=torch.uint8)
+        full = parallel.allgather_tables(host)
+        out[(rank, k)] = full.numpy().tobytes() == tb
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_gloo_sharded_table_upload_reassembles_the_set(world):
+    """Each rank contributes only its 1/G slice of the host tables; every rank
+    ends up with the byte-identical set (the e2e multi-GPU upload path)."""
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_gather_worker, args=(world, _free_port(), out), nprocs=world, join=True)
+    assert len(out) == 2 * world and all(out.values())
+
+
 def _free_port():
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
