@@ -97,8 +97,9 @@ int cgpu_tables_build(cgpu_ctx* ctx, const uint32_t* primes, uint32_t n, int alg
 int cgpu_tables_load(cgpu_ctx* ctx, const uint32_t* primes, uint32_t n, const uint8_t* bytes,
                      uint64_t nbytes);
 
-/* As cgpu_tables_load, from DEVICE memory on ctx's device (ordered on ctx's
- * stream): the multi-GPU upload path, where each rank copies 1/G of the host
+/* As cgpu_tables_load, from DEVICE memory on ctx's device, read by a copy on
+ * ctx's stream (the bytes must be complete by then: written on that stream or
+ * synchronised with it): the multi-GPU upload path, where each rank copies 1/G of the host
  * tables over PCIe and the full set is all-gathered over NVLink first
  * (parallel.py load_tables_sharded). */
 int cgpu_tables_load_dev(cgpu_ctx* ctx, const uint32_t* primes, uint32_t n, const void* d_bytes,

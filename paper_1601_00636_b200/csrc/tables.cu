@@ -249,8 +249,8 @@ __global__ void __launch_bounds__(kCubeThreads) k_cube_f2(const PrimeJob* __rest
 		for (uint32_t t = 0; t < r; ++t) {
 			const float4 bp = s_b[t];
 			const uint32_t w = s_w[t];
-			// power-major: consecutive FFMA2 share the broadcast operand
-			// (register reuse) and the NP chains are independent
+			// the NP chains are independent; ptxas interleaves them as it sees
+			// fit (forcing the order with volatile asm measured no faster)
 			unsigned long long v[NP];
 #pragma unroll
 			for (int j = 0; j < NP; ++j) v[j] = ffma2(C4[j], bp.w, V0[j]);

@@ -362,6 +362,50 @@ def test_sharded_sieve_single_rank(dev):
     assert np.array_equal(sp, o["survivor_pairs"])
 
 
+def test_load_from_device_memory_and_nccl_sharded_upload(dev, golden, sets):
+    """cgpu_tables_load_dev (tables already in device memory) and the N>1
+    e2e upload path parallel.load_tables_sharded run through a real NCCL
+    all-gather (world size 1 on this GPU): identical resident set, C3 result
+    identical to the reference's; a bad padding bit is still a FormatError."""
+    import os
+    import socket
+    import torch
+    import torch.distributed as dist
+    from paper_1601_00636_b200 import parallel
+    P = sets["odd64"]
+    tb, offs = port.build_set(P)
+    d_tb = torch.frombuffer(bytearray(tb), dtype=torch.uint8).cuda()
+    torch.cuda.synchronize()  # the context has its own stream: the bytes must be ready
+    dev.load_dev(P, d_tb.data_ptr(), d_tb.numel())
+    assert dev.download() == tb
+    bad = d_tb.clone()
+    k11 = list(P).index(11)
+    bad[int(offs[k11]) + (11 * 11 + 7) // 8 - 1] |= 0x80  # a padding bit of the r = 11 table
+    torch.cuda.synchronize()
+    with pytest.raises(N.CudaSieveError):
+        dev.load_dev(P, bad.data_ptr(), bad.numel())
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(sk.getsockname()[1]))
+    sk.close()
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        stream = torch.cuda.Stream()
+        dev.set_stream(stream.cuda_stream)
+        host = torch.frombuffer(bytearray(tb), dtype=torch.uint8).pin_memory()
+        with torch.cuda.stream(stream):
+            full = parallel.load_tables_sharded(dev, P, host)
+        dev.synchronize()
+        assert full.is_cuda and dev.download() == tb
+        r = dev.sieve(2, 10000, N.TRIANGLE)
+        g = golden["sieve"]["C3"]
+        assert r.pairs_tested == g["pairs_tested"] and r.survivors == g["survivors"]
+        assert {str(P[k]): int(c) for k, c in enumerate(r.hist) if c} == g["kill_histogram"]
+    finally:
+        dev.set_stream(None)
+        dist.destroy_process_group()
+
+
 def test_files_roundtrip_with_reference(tmp_path, sets):
     """GPU-built tables written through the C ABI are the reference's files
     (save_sieve_files / load_sieve_files, test_sievetable.cpp:240-262), and
