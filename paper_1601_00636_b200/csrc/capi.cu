@@ -145,6 +145,7 @@ struct cgpu_ctx {
 	uint32_t reg_r[kMaxReg] = {}, reg_m[kMaxReg] = {}, reg_base[kMaxReg] = {}, reg_delta[kMaxReg] = {};
 	uint32_t reg_tab[kMaxReg] = {}, wtab_n = 0;
 	DevBuf<uint4> d_tabprobes;
+	DevBuf<uint4> derive_items;
 	DevBuf<uint32_t> wintab;
 	int grid = 0;
 	std::map<uint64_t, int> grid_cache;
@@ -316,9 +317,12 @@ int finalize_set(cgpu_ctx* c, bool check_padding = false)
 		CK(cudaMemcpyAsync(c->d_offsets.p, c->offsets.data(), 4ull * n, cudaMemcpyHostToDevice,
 		                   c->stream));
 		CK(cudaMemsetAsync(c->killflags.p, 0, 4ull * n, c->stream));
-		uint64_t max_words = 0;
-		for (auto r : c->primes) max_words = std::max<uint64_t>(max_words, uint64_t(r) * ext_row_words(r));
-		CK(launch_derive(c->jobs_rank.p, n, max_words, c->packed.p, c->ext.p, c->killflags.p, c->stream));
+		const std::vector<uint4> items = derive_items(c->primes);
+		CK(c->derive_items.ensure(items.size()));
+		CK(cudaMemcpyAsync(c->derive_items.p, items.data(), sizeof(uint4) * items.size(), cudaMemcpyHostToDevice,
+		                   c->stream));
+		CK(launch_derive(c->jobs_rank.p, c->derive_items.p, static_cast<uint32_t>(items.size()), c->packed.p,
+		                 c->ext.p, c->killflags.p, c->stream));
 		++c->launches;
 	}
 	std::vector<uint32_t> kf(n + 1, 0);

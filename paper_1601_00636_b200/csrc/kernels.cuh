@@ -3,6 +3,7 @@
 
 #include <cstdint>
 #include <cuda_runtime.h>
+#include <vector>
 
 namespace cgpu {
 
@@ -34,16 +35,17 @@ cudaError_t launch_permute(const PrimeJob* d_jobs, uint32_t njobs, uint32_t max_
                            cudaStream_t s);
 
 // Packed reference bytes -> row-extended words + killable flags; jobs in rank
-// order (killable index = blockIdx.y). max_words = largest r * ext_row_words(r).
+// order (killable index = job), one CTA per work item (derive_items).
 // Window tables of the table probes (k_sieve's first kTabProbes register
 // probes) for every row: probes[j] = {r, ext_base, S, tab base}; out holds
 // `stride` masks then `stride` successor indices.
 cudaError_t launch_wintab(const uint4* d_probes, uint32_t nprobes, uint32_t entries, const uint32_t* d_ext,
                           uint32_t stride, uint32_t* d_out, cudaStream_t s);
 
-cudaError_t launch_derive(const PrimeJob* d_jobs, uint32_t njobs, uint64_t max_words,
-                          const uint8_t* d_packed, uint32_t* d_ext, uint32_t* d_killable,
-                          cudaStream_t s);
+cudaError_t launch_derive(const PrimeJob* d_jobs, const uint4* d_items, uint32_t nitems, const uint8_t* d_packed,
+                          uint32_t* d_ext, uint32_t* d_killable, cudaStream_t s);
+// k_derive work items {job, first row, rows, 0} of <= kDeriveItemWords output words each
+std::vector<uint4> derive_items(const std::vector<uint32_t>& primes);
 
 // Padding-bit check for uploaded tables (FormatError on nonzero padding).
 cudaError_t launch_check_padding(const PrimeJob* d_jobs, uint32_t njobs, const uint8_t* d_packed,
@@ -56,6 +58,7 @@ constexpr uint32_t kCubeF2MaxR = 2039;  // largest prime with h + 4h^2 < 2^22, h
 constexpr uint32_t kPermThreads = 256;
 constexpr uint32_t kRow1Threads = 128;
 constexpr uint32_t kDeriveThreads = 256;
+constexpr uint32_t kDeriveItemWords = 2048;  // output words per k_derive CTA
 
 // ---- K2: sieve ---------------------------------------------------------------
 

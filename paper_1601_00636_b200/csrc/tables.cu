@@ -13,6 +13,9 @@
 #include "common.cuh"
 #include "kernels.cuh"
 
+#include <algorithm>
+#include <vector>
+
 namespace cgpu {
 namespace {
 
@@ -341,30 +344,42 @@ __global__ void __launch_bounds__(kPermThreads) k_permute(const PrimeJob* __rest
 }
 
 // Packed reference tables -> row-extended words (common.cuh ext_row_words):
-// word j of row a holds bits u(a, (32j + l) mod r), l = 0..31. One thread per
-// word gathers its 32 bits from the packed row (L1-resident bytes);
-// killable[k] is set when any word of table k is nonzero.
+// word j of row a holds bits u(a, (32j + l) mod r), l = 0..31. One CTA per
+// work item {job, first row, rows} (built on the host, <= kDeriveItemWords
+// output words each): the CTA stages the item's packed bits in shared memory
+// with coalesced word loads, then each thread builds output words from it
+// (one or two funnel shifts across the row wrap) and stores them coalesced;
+// killable[k] is set when any word of table k is nonzero. (Per-word gathers
+// straight from L2 were latency-bound: 113-145 us for the 256-prime set.)
 __global__ void __launch_bounds__(kDeriveThreads) k_derive(const PrimeJob* __restrict__ jobs,
+                                                           const uint4* __restrict__ items,
                                                            const uint8_t* __restrict__ packed,
                                                            uint32_t* __restrict__ ext,
                                                            uint32_t* __restrict__ killable)
 {
-	const PrimeJob job = jobs[blockIdx.y];
+	extern __shared__ uint32_t s_bits[];
+	const uint4 it = items[blockIdx.x];  // {job, first row, rows, -}
+	const PrimeJob job = jobs[it.x];
 	const uint32_t r = job.r, m = job.m, S = ext_row_words(r);
-	const uint32_t words = r * S;
-	const uint8_t* tab = packed + job.byte_off;
-	const uint32_t mS = barrett_m(S);
-	bool any = false;
-	// 32 bits of the packed bitstream starting at bit i (any alignment), from
-	// the two aligned little-endian words around it
-	const uint64_t base_bits = 8ull * job.byte_off;
+	// global bit range of the rows, staged from its first aligned word
+	const uint64_t bit0 = 8ull * job.byte_off + static_cast<uint64_t>(it.y) * r;
+	const uint64_t w0 = bit0 >> 5;
+	const uint32_t nbits = it.z * r;
+	const uint32_t nw = static_cast<uint32_t>((((bit0 & 31) + nbits + 31) >> 5) + 1);
 	const uint32_t* words32 = reinterpret_cast<const uint32_t*>(packed);
-	auto bits32 = [&](uint64_t i) {
-		const uint64_t g = base_bits + i;
-		return __funnelshift_r(__ldg(words32 + (g >> 5)), __ldg(words32 + (g >> 5) + 1), static_cast<uint32_t>(g & 31));
+	for (uint32_t i = threadIdx.x; i < nw; i += blockDim.x) s_bits[i] = __ldg(words32 + w0 + i);
+	__syncthreads();
+	const uint32_t sh = static_cast<uint32_t>(bit0 & 31);  // bit offset of row it.y in s_bits
+	// 32 bits starting at local bit i of the staged rows
+	auto bits32 = [&](uint32_t i) {
+		const uint32_t li = i + sh;
+		return __funnelshift_r(s_bits[li >> 5], s_bits[(li >> 5) + 1], li & 31);
 	};
-	for (uint32_t w = blockIdx.x * blockDim.x + threadIdx.x; w < words; w += gridDim.x * blockDim.x) {
-		uint32_t a = __umulhi(w, mS), j = w - a * S;  // w / S, w % S
+	bool any = false;
+	const uint32_t words = it.z * S;
+	const uint32_t mS = barrett_m(S);
+	for (uint32_t w = threadIdx.x; w < words; w += blockDim.x) {
+		uint32_t a = __umulhi(w, mS), j = w - a * S;  // local row, word in row
 		if (j >= S) { j -= S; ++a; }
 		uint32_t b = mod_full(32 * j, r, m);  // offset of bit 0 of the word in the row
 		const uint32_t row0 = a * r;
@@ -374,18 +389,18 @@ __global__ void __launch_bounds__(kDeriveThreads) k_derive(const PrimeJob* __res
 			word = bits32(row0 + b);
 			if (head < 32) word = (word & ((1u << head) - 1)) | (bits32(row0) << head);
 		} else {  // small r: the row repeats inside one word
+			const uint32_t row = bits32(row0) & ((1u << r) - 1);
 			word = 0;
 #pragma unroll 8
 			for (uint32_t l = 0; l < 32; ++l) {
-				const uint32_t idx = row0 + b;
-				word |= ((__ldg(tab + (idx >> 3)) >> (idx & 7)) & 1u) << l;
+				word |= ((row >> b) & 1u) << l;
 				b = b + 1 == r ? 0 : b + 1;
 			}
 		}
-		ext[job.ext_base + w] = word;
+		ext[job.ext_base + static_cast<uint64_t>(it.y) * S + w] = word;
 		any |= word != 0;
 	}
-	if (__any_sync(kFull, any) && (threadIdx.x & 31) == 0) atomicOr(&killable[blockIdx.y], 1u);
+	if (__syncthreads_or(any) && threadIdx.x == 0) atomicOr(&killable[it.x], 1u);
 }
 
 // Window tables for the sieve's table probes: entry (j, a, b) -- for probe j
@@ -498,14 +513,25 @@ cudaError_t launch_wintab(const uint4* d_probes, uint32_t nprobes, uint32_t entr
 	return cudaGetLastError();
 }
 
-cudaError_t launch_derive(const PrimeJob* d_jobs, uint32_t njobs, uint64_t max_words,
-                          const uint8_t* d_packed, uint32_t* d_ext, uint32_t* d_killable,
-                          cudaStream_t s)
+cudaError_t launch_derive(const PrimeJob* d_jobs, const uint4* d_items, uint32_t nitems, const uint8_t* d_packed,
+                          uint32_t* d_ext, uint32_t* d_killable, cudaStream_t s)
 {
-	if (!njobs) return cudaSuccess;
-	const dim3 grid(grid_x(max_words, kDeriveThreads, 1024), njobs);
-	k_derive<<<grid, kDeriveThreads, 0, s>>>(d_jobs, d_packed, d_ext, d_killable);
+	if (!nitems) return cudaSuccess;
+	// staged bits: <= kDeriveItemWords output words cover <= kDeriveItemWords * 32 bits... plus slack
+	const size_t smem = sizeof(uint32_t) * (kDeriveItemWords + 4);
+	k_derive<<<nitems, kDeriveThreads, smem, s>>>(d_jobs, d_items, d_packed, d_ext, d_killable);
 	return cudaGetLastError();
+}
+
+std::vector<uint4> derive_items(const std::vector<uint32_t>& primes)
+{
+	std::vector<uint4> items;
+	for (uint32_t k = 0; k < primes.size(); ++k) {
+		const uint32_t r = primes[k], S = ext_row_words(r);
+		const uint32_t R = std::max<uint32_t>(1, kDeriveItemWords / S);  // rows per item
+		for (uint32_t a = 0; a < r; a += R) items.push_back(make_uint4(k, a, std::min(R, r - a), 0));
+	}
+	return items;
 }
 
 cudaError_t launch_check_padding(const PrimeJob* d_jobs, uint32_t njobs, const uint8_t* d_packed,
