@@ -51,7 +51,7 @@ WORKLOADS = {
     "C3": dict(k=64, p_lo=2, p_hi=10000, pairs=30397485,
                desc="C3: TRIANGLE sieve p<=1e4, 1<=q<p coprime, 64 odd primes 3..313"),
 }
-GATHER_CAP = 1024  # survivors per rank gathered inside the step (C1..C5 have 0; overflow is counted)
+GATHER_CAP = 128  # survivors per rank gathered inside the step (C1..C5 have 0; overflow fails parity)
 
 
 # ---- host-side workload constants ------------------------------------------------------
@@ -477,6 +477,10 @@ def run_ours(args, wl, primes):
             C.c_void_p(acc.data_ptr()), C.c_void_p(acc.data_ptr() + 16), C.c_void_p(brm.data_ptr()),
             nblocks, C.c_void_p(surv_mine.data_ptr()), GATHER_CAP))
         local_pairs = int(acc[0].item())
+        overflow = allreduce_max(float(int(acc[1].item()) > GATHER_CAP)) > 0
+    else:
+        overflow = survivors > GATHER_CAP
+    parity_ok = parity_ok and not overflow  # every survivor must have been gathered
     opp, d_eff, omega_bar = ops_per_pair(primes, killable, hist, survivors, pairs,
                                          wl["p_lo"], wl["p_hi"])
     kavg = float(np.mean(kern_ms))
