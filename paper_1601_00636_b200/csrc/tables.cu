@@ -349,7 +349,9 @@ __global__ void __launch_bounds__(kPermThreads) k_permute(const PrimeJob* __rest
 // output words each): the CTA stages the item's packed bits in shared memory
 // with coalesced word loads, then each thread builds output words from it
 // (one or two funnel shifts across the row wrap) and stores them coalesced;
-// killable[k] is set when any word of table k is nonzero. (Per-word gathers
+// killable[k] is set when any word of table k is nonzero. Row 0 is written as
+// zeros whatever the bytes hold: scan() skips primes with p mod r = 0
+// (engine.hpp:240-242), and canonical tables have a zero row 0 anyway. (Per-word gathers
 // straight from L2 were latency-bound: 113-145 us for the 256-prime set.)
 __global__ void __launch_bounds__(kDeriveThreads) k_derive(const PrimeJob* __restrict__ jobs,
                                                            const uint4* __restrict__ items,
@@ -397,6 +399,7 @@ __global__ void __launch_bounds__(kDeriveThreads) k_derive(const PrimeJob* __res
 				b = b + 1 == r ? 0 : b + 1;
 			}
 		}
+		if (it.y + a == 0) word = 0;  // row p = 0 mod r: scan() never probes it (engine.hpp:240-242)
 		ext[job.ext_base + static_cast<uint64_t>(it.y) * S + w] = word;
 		any |= word != 0;
 	}

@@ -216,6 +216,30 @@ def test_random_ranges_vs_oracle(dev, seed):
             assert got == want
 
 
+@pytest.mark.parametrize("prime,flip", [(11, (2, 5)), (13, (0, 4)), (13, (7, 12))])
+def test_non_canonical_tables_vs_oracle(dev, prime, flip):
+    """Tables loaded from bytes the reference's builder would never produce
+    (one flipped bit of a row a >= 1, which breaks u(la, lb) = u(a, b), or of
+    row 0) must still sieve exactly like the reference's scan(): the kernel
+    reads the bits as loaded and, like engine.hpp:240-242, never probes row
+    0 (k_derive writes it as zeros)."""
+    P = odd_primes(96)
+    tb, offs = port.build_set(P)
+    k = P.index(prime)
+    a, b = flip
+    i = a * prime + b
+    bad = bytearray(tb)
+    bad[int(offs[k]) + (i >> 3)] ^= 1 << (i & 7)
+    bad = bytes(bad)
+    dev.load(P, bad)
+    for lo, hi, mode in ((2, 3000, N.TRIANGLE), (152, 700, N.REGION)):
+        o = port.sieve(bad, P, offs, lo, hi, mode)
+        r = dev.sieve(lo, hi, mode, surv_cap=1 << 22)
+        assert (r.pairs_tested, r.survivors) == (o["pairs_tested"], o["survivors"])
+        assert r.hist.tolist() == o["hist"].tolist()
+        assert np.array_equal(r.survivor_pairs, o["survivor_pairs"])
+
+
 REG_LAYOUTS = [
     # (prime set, CUBOID_REG3_PROBES, CUBOID_NO_STD_PRIMES): every register /
     # window-table probe layout the context can choose (capi.cu finalize_set)
