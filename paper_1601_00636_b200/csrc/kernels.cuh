@@ -105,7 +105,8 @@ constexpr uint32_t kTabStrideStd = std_tab_entries(7 + kStdReg3 < kTabProbes ? 7
 constexpr uint32_t kTabStrideGen = kTabStrideStd > 7424 ? kTabStrideStd : 7424;
 constexpr int kQueue = 64;      // per-warp deep-probe work queue entries
 constexpr uint32_t kPlanChunk = 1024;  // row slots per plan CTA
-constexpr uint32_t kFacWords = 1 + kMaxFactors;  // per row slot: nf | even << 8, odd factors
+// per row slot: nf | even << 8, the odd factors, then their Barrett constants
+constexpr uint32_t kFacWords = 1 + 2 * kMaxFactors;
 
 struct SieveArgs {
 	const uint32_t* ext;          // row-extended tables

@@ -169,7 +169,8 @@ __device__ __forceinline__ unsigned long long block_excl_scan(unsigned long long
 // multiples of f, then each row divides its marked primes out and what is
 // left of p is 1 or its single prime factor above sqrt(p). Output per slot:
 // out[0] = nf | even << 8, out[1..nf] = the odd prime factors that can divide
-// some q of the row (<= qhi), ascending. Empty rows get nf = 0.
+// some q of the row (<= qhi), ascending, out[1 + kMaxFactors + i] = the
+// Barrett constant of factor i. Empty rows get nf = 0.
 struct PlanSmem {
 	uint32_t nf[kPlanChunk];
 	uint16_t fi[kPlanChunk][kMaxFactors];  // indices into a.fprimes
@@ -221,12 +222,20 @@ __device__ __forceinline__ void factorise_chunk(const SieveArgs& a, PlanSmem& sm
 				if (r) break;
 				cof = qt;
 			}
-			if (fp.x == 2) even = 1;
-			else if (fp.x <= rb.qhi && nf < kMaxFactors) out[1 + nf++] = fp.x;
+			if (fp.x == 2) {
+				even = 1;
+			} else if (fp.x <= rb.qhi && nf < kMaxFactors) {
+				out[1 + kMaxFactors + nf] = fp.y;
+				out[1 + nf++] = fp.x;
+			}
 		}
 		if (cof > 1) {  // the prime factor above sqrt(p)
-			if (cof == 2) even = 1;
-			else if (cof <= rb.qhi && nf < kMaxFactors) out[1 + nf++] = cof;
+			if (cof == 2) {
+				even = 1;
+			} else if (cof <= rb.qhi && nf < kMaxFactors) {
+				out[1 + kMaxFactors + nf] = static_cast<uint32_t>((1ull << 32) / cof);
+				out[1 + nf++] = cof;
+			}
 		}
 	}
 	out[0] = nf | (even << 8);
@@ -272,6 +281,14 @@ __global__ void __launch_bounds__(kPlanChunk) k_plan(const SieveArgs a)
 		a.tickets[0] = 0;  // ready for the next launch on this stream
 	}
 }
+
+// period_mask(f) for f < 32 (bits at 0, f, 2f, ...): read by a whole warp
+// at one index (the row's factor), so the constant bank broadcasts it
+__constant__ uint32_t c_period_mask[32] = {
+    0u,          0xffffffffu, 0x55555555u, 0x49249249u, 0x11111111u, 0x42108421u, 0x41041041u, 0x10204081u,
+    0x01010101u, 0x08040201u, 0x40100401u, 0x00400801u, 0x01001001u, 0x04002001u, 0x10004001u, 0x40008001u,
+    0x00010001u, 0x00020001u, 0x00040001u, 0x00080001u, 0x00100001u, 0x00200001u, 0x00400001u, 0x00800001u,
+    0x01000001u, 0x02000001u, 0x04000001u, 0x08000001u, 0x10000001u, 0x20000001u, 0x40000001u, 0x80000001u};
 
 #ifdef CGPU_DEBUG
 __device__ __forceinline__ uint32_t dynamic_smem_size()
@@ -384,6 +401,7 @@ struct RowCtx {
 	uint32_t p, qlo, qhi, w0, w1, wlast, tail, even;
 	uint32_t nf;
 	uint32_t fac[kMaxFactors];  // odd prime factors of p that can divide some q of the row
+	uint32_t fm[kMaxFactors];   // their Barrett constants
 };
 
 // Warp-collective: the number of q in [qa, qb] coprime to p, by
@@ -430,12 +448,14 @@ __device__ __forceinline__ uint32_t row_loop(const SieveArgs& a, const WarpSmem&
 #pragma unroll
 	for (int k = 0; k < NF; ++k) {
 		if (k < static_cast<int>(rc.nf)) {
-			const uint32_t f = rc.fac[k];
-			const uint32_t b = q0_first % f;
+			// Barrett remainders (the factor's constant from k_plan; f < 2^31 so
+			// the lazy remainder stays below 2^32) and a constant-bank mask
+			const uint32_t f = rc.fac[k], m = rc.fm[k];
+			const uint32_t b = mod_full(q0_first, f, m);
 			ff[k] = f;
 			fo[k] = b ? f - b : 0;
-			fd[k] = kStepQ % f;
-			fpat[k] = period_mask(f);
+			fd[k] = mod_full(kStepQ, f, m);
+			fpat[k] = f < 32 ? c_period_mask[f] : 1u;
 		} else {  // padding slot of a wider variant: contributes no bits
 			ff[k] = 1;
 			fo[k] = fd[k] = fpat[k] = 0;
@@ -661,7 +681,10 @@ __global__ void __launch_bounds__(kSieveThreads, kSieveMinBlocks) k_sieve(const 
 		rc.nf = head & 0xffu;
 		const bool even = (head >> 8) & 1u;
 #pragma unroll
-		for (int k = 0; k < kMaxFactors; ++k) rc.fac[k] = __shfl_sync(kFull, fw, k + 1);
+		for (int k = 0; k < kMaxFactors; ++k) {
+			rc.fac[k] = __shfl_sync(kFull, fw, k + 1);
+			rc.fm[k] = __shfl_sync(kFull, fw, k + 1 + kMaxFactors);
+		}
 		// q0 parity is fixed per lane (q advances by 32 per window): even p
 		// excludes the even q of every window
 		rc.even = even ? (((rc.qlo + 32 * (rc.w0 + lane)) & 1) ? 0xAAAAAAAAu : 0x55555555u) : 0u;
