@@ -296,6 +296,12 @@ def run_ours(args, wl, primes):
                      "peak": fp_peak["cube_mix_evals"], "unit": "evals/s",
                      "frac": tb_evals / (cube_ms * 1e-3) / fp_peak["cube_mix_evals"],
                      "fp32_peaks": fp_peak,
+                     # the same bound from the pipes alone: 2 FFMA2 + 1 IMAD per eval
+                     # issued at their separately measured chain rates
+                     "fma_pipe_model_evals": 1.0 / (2.0 / (fp_peak["ffma2_lane_fmas"] / 2)
+                                                    + 1.0 / int_peak["fma_imad"]),
+                     "frac_vs_fma_pipe_model": tb_evals / (cube_ms * 1e-3) / (
+                         1.0 / (2.0 / (fp_peak["ffma2_lane_fmas"] / 2) + 1.0 / int_peak["fma_imad"])),
                      "imad_path_peak_evals": int_peak["fma_imad"] / 5,
                      "horner_ops_per_eval_survey": 27,
                      "note": "SURVEY 8(d) counts 27 INT32 ops/eval for Horner; the kernel issues 4 "
