@@ -151,6 +151,7 @@ struct cgpu_ctx {
 	std::map<uint64_t, int> grid_cache;
 
 	uint32_t row_cost = kDefaultRowCost;
+	float drain_alpha = kDefaultDrainAlpha;
 	DevBuf<uint2> fprimes;
 	uint32_t n_fprimes = 0;
 
@@ -215,6 +216,7 @@ int cgpu_create(int device, void* stream, cgpu_ctx** out)
 	}
 	cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device);
 	if (const char* rc = std::getenv("CUBOID_ROW_COST")) c->row_cost = static_cast<uint32_t>(std::atoi(rc));
+	if (const char* da = std::getenv("CUBOID_DRAIN_ALPHA")) c->drain_alpha = static_cast<float>(std::atof(da));
 	for (auto& e : c->ev) cudaEventCreate(&e);
 	// trial-division primes below 2^16 (covers sqrt of any p < 2^32)
 	std::vector<uint2> fp;
@@ -768,6 +770,7 @@ int enqueue_sieve(cgpu_ctx* c, uint64_t p_lo, uint64_t q_start, uint64_t p_hi, u
 	a.fprimes = c->fprimes.p;
 	a.n_fprimes = c->n_fprimes;
 	a.row_cost = c->row_cost;
+	a.drain_alpha = c->drain_alpha;
 	a.p_lo = p_lo;
 	a.p_hi = p_hi;
 	a.q_start = q_start;

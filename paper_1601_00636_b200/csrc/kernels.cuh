@@ -105,8 +105,10 @@ constexpr uint32_t kTabStrideStd = std_tab_entries(7 + kStdReg3 < kTabProbes ? 7
 constexpr uint32_t kTabStrideGen = kTabStrideStd > 7424 ? kTabStrideStd : 7424;
 constexpr int kQueue = 64;      // per-warp deep-probe work queue entries
 constexpr uint32_t kPlanChunk = 1024;  // row slots per plan CTA
-// per row slot: nf | even << 8, the odd factors, then their Barrett constants
+// per row slot: nf | even << 8 | window-weight shift << 16, the odd factors,
+// then their Barrett constants
 constexpr uint32_t kFacWords = 1 + 2 * kMaxFactors;
+constexpr float kDefaultDrainAlpha = 8.0f;
 
 struct SieveArgs {
 	const uint32_t* ext;          // row-extended tables
@@ -132,6 +134,7 @@ struct SieveArgs {
 	uint64_t blk0;                // first owned block of this launch
 	uint32_t n_slots;
 	uint32_t row_cost;            // load-balance charge per row (window-equivalents)
+	float drain_alpha;            // load-balance weight of a window queued for the deep probes
 	// work units before slot s = prefix[s] + chunk_off[s / kPlanChunk]
 	unsigned long long* prefix;        // [n_slots + 1] (chunk-local exclusive scan)
 	unsigned long long* chunk_off;     // [n_chunks + 1] (exclusive scan of chunk totals)

@@ -122,10 +122,32 @@ __device__ __forceinline__ uint64_t row_windows(const RowBounds& b)
 // charge a.row_cost for the per-row setup (factor masks, register-probe rows,
 // the row-end queue drain and counts). Without it the warps that own the many
 // short rows at small p straggle (C4: one SM busy 5x longer than the rest).
-__device__ __forceinline__ uint64_t row_units(const SieveArgs& a, const RowBounds& b)
+//
+// Windows are weighted by the expected share queued for the deep probes: the
+// register probes kill a fixed fraction k_j of any row's pairs except when
+// r_j | p (row 0 never kills), so rows that several of 11..37 divide keep up
+// to ~100x more survivors (C5: median s = 3.3e-4 alive after the register
+// probes, max 3.7e-2) and drain most of their windows. Unweighted, the warps
+// that drew such a row ran on alone for up to +50% -- the whole tail of a
+// launch with few rows per warp (a shard of 8 ranks). Weight = 1 + alpha
+// (1 - exp(-c s)) (c = the window's coprime candidates, alpha =
+// a.drain_alpha window-equivalents per queued window), rounded to a power of
+// two 2^shift (shift <= 3, stored in the row's factor head) so that mapping
+// units back to windows is a shift.
+__device__ __forceinline__ uint64_t row_units(const SieveArgs& a, const RowBounds& b, uint32_t shift)
 {
 	const uint64_t w = row_windows(b);
-	return w ? w + a.row_cost : 0;
+	return w ? a.row_cost + (w << shift) : 0;
+}
+
+// First window of the row at unit u (the inverse of row_units; monotonic, so
+// adjacent warps' unit slices map to adjacent window ranges).
+__device__ __forceinline__ uint32_t unit_window(const SieveArgs& a, unsigned long long u, uint32_t shift,
+                                                uint32_t windows)
+{
+	if (u <= a.row_cost) return 0;
+	const unsigned long long w = (u - a.row_cost + (1u << shift) - 1) >> shift;
+	return static_cast<uint32_t>(w < windows ? w : windows);
 }
 
 __device__ __forceinline__ unsigned long long slot_prefix(const SieveArgs& a, uint32_t s)
@@ -172,15 +194,23 @@ __device__ __forceinline__ unsigned long long block_excl_scan(unsigned long long
 // some q of the row (<= qhi), ascending, out[1 + kMaxFactors + i] = the
 // Barrett constant of factor i. Empty rows get nf = 0.
 struct PlanSmem {
+	float kill[kMaxReg];  // kill fraction of a nonzero row of register probe j
 	uint32_t nf[kPlanChunk];
 	uint16_t fi[kPlanChunk][kMaxFactors];  // indices into a.fprimes
 };
 
-__device__ __forceinline__ void factorise_chunk(const SieveArgs& a, PlanSmem& sm, uint32_t c0, const RowBounds& rb,
-                                                uint32_t* out)
+__device__ __forceinline__ uint32_t factorise_chunk(const SieveArgs& a, PlanSmem& sm, uint32_t c0,
+                                                    const RowBounds& rb, uint32_t* out)
 {
 	const uint32_t t = threadIdx.x;
 	sm.nf[t] = 0;
+	if (t < a.nreg) {  // row 1 of the probe (canonical rows a >= 1 share its popcount)
+		const uint32_t r = a.reg_r[t], S = ext_row_words(r);
+		const uint32_t* row = a.ext + a.reg_base[t] + S;
+		const uint32_t lo = r < 32 ? (1u << r) - 1 : 0xffffffffu;
+		const uint32_t n = __popc(row[0] & lo) + (r > 32 ? __popc(row[1] & ((1u << (r - 32)) - 1)) : 0);
+		sm.kill[t] = static_cast<float>(n) / static_cast<float>(r);
+	}
 	// largest row of the chunk (slots ascend in p)
 	const uint32_t s_last = min(c0 + kPlanChunk, a.n_slots) - 1;
 	const uint64_t p_last = (a.blk0 + static_cast<uint64_t>(s_last / 100) * a.G) * 100 + s_last % 100;
@@ -202,7 +232,7 @@ __device__ __forceinline__ void factorise_chunk(const SieveArgs& a, PlanSmem& sm
 		}
 	}
 	__syncthreads();
-	if (c0 + t >= a.n_slots) return;
+	if (c0 + t >= a.n_slots) return 0;
 	uint32_t nf = 0, even = 0;
 	if (rb.qhi >= rb.qlo && rb.p > 1) {
 		const uint32_t n = min(sm.nf[t], static_cast<uint32_t>(kMaxFactors));
@@ -239,6 +269,17 @@ __device__ __forceinline__ void factorise_chunk(const SieveArgs& a, PlanSmem& sm
 		}
 	}
 	out[0] = nf | (even << 8);
+	// window weight (row_units): survival after the register probes that do
+	// not divide p, times the row's coprime candidates per window
+	float surv = 1.0f, cop = even ? 0.5f : 1.0f;
+	const uint32_t p32 = static_cast<uint32_t>(rb.p);
+	for (uint32_t j = 0; j < a.nreg; ++j)
+		if (p32 % a.reg_r[j]) surv *= 1.0f - sm.kill[j];
+	for (uint32_t j = 0; j < nf; ++j) cop *= 1.0f - 1.0f / static_cast<float>(out[1 + j]);
+	const float wt = 1.0f + a.drain_alpha * (1.0f - __expf(-32.0f * cop * surv));
+	const uint32_t shift = wt >= 6.0f ? 3u : wt >= 3.0f ? 2u : wt >= 1.5f ? 1u : 0u;
+	out[0] |= shift << 16;
+	return shift;
 }
 
 // Plan: per row slot, the work units before it. Each CTA scans kPlanChunk
@@ -257,8 +298,9 @@ __global__ void __launch_bounds__(kPlanChunk) k_plan(const SieveArgs a)
 		if (s < 2) a.counters[s] = 0;
 	}
 	const RowBounds rb = s < n ? slot_row(a, s) : RowBounds{0, 1, 0};
-	const unsigned long long u = s < n ? row_units(a, rb) : 0;
-	factorise_chunk(a, s_fac, blockIdx.x * kPlanChunk, rb, a.rowfac + static_cast<size_t>(s) * kFacWords);
+	const uint32_t shift = factorise_chunk(a, s_fac, blockIdx.x * kPlanChunk, rb,
+	                                       a.rowfac + static_cast<size_t>(s) * kFacWords);
+	const unsigned long long u = s < n ? row_units(a, rb, shift) : 0;
 	unsigned long long total;
 	const unsigned long long ex = block_excl_scan(u, s_warp, total);
 	if (s < n) a.prefix[s] = ex;
@@ -656,7 +698,7 @@ __global__ void __launch_bounds__(kSieveThreads, kSieveMinBlocks) k_sieve(const 
 			continue;
 		}
 		// this warp's share of the row's units; the first row_cost are the
-		// setup charge, the rest map 1:1 to windows
+		// setup charge, the rest map to windows (unit_window)
 		const unsigned long long u0 = ws - rs, u1 = min(we, re) - rs;
 		ws = min(we, re);
 		const uint32_t cur = slot++;
@@ -668,8 +710,6 @@ __global__ void __launch_bounds__(kSieveThreads, kSieveMinBlocks) k_sieve(const 
 		rc.qlo = static_cast<uint32_t>(rb.qlo);
 		const uint32_t qhi = static_cast<uint32_t>(rb.qhi);
 		rc.qhi = qhi;
-		rc.w0 = static_cast<uint32_t>(u0 > rcost ? u0 - rcost : 0);
-		rc.w1 = static_cast<uint32_t>(u1 - rcost);
 		rc.wlast = (qhi - rc.qlo) / 32;
 		rc.tail = (2u << (qhi - (rc.qlo + 32 * rc.wlast))) - 1;  // span 31 -> all ones
 
@@ -680,6 +720,11 @@ __global__ void __launch_bounds__(kSieveThreads, kSieveMinBlocks) k_sieve(const 
 		const uint32_t head = __shfl_sync(kFull, fw, 0);
 		rc.nf = head & 0xffu;
 		const bool even = (head >> 8) & 1u;
+		// this warp's windows of the row (row_units / unit_window)
+		rc.w0 = unit_window(a, u0, (head >> 16) & 3u, rc.wlast + 1);
+		rc.w1 = unit_window(a, u1, (head >> 16) & 3u, rc.wlast + 1);
+		if (rc.w1 <= rc.w0) continue;
+
 #pragma unroll
 		for (int k = 0; k < kMaxFactors; ++k) {
 			rc.fac[k] = __shfl_sync(kFull, fw, k + 1);

@@ -13,11 +13,13 @@ from paper_1601_00636_b200 import device as D, _native as N, odd_primes  # noqa:
 cfg = {"C3": (64, 2, 10000), "C4": (128, 2, 100000), "C5": (256, 100001, 300000)}
 dev = D.Device(0)
 L = N.lib()
-for name in sys.argv[1].split(","):
+for spec in sys.argv[1].split(","):  # NAME or NAME/G/g (block-cyclic shard g of G)
+    name, *sh = spec.split("/")
+    shard = (int(sh[0]), int(sh[1])) if sh else (1, 0)
     k, lo, hi = cfg[name]
     dev.build(odd_primes(k), N.BUILD_PRODUCTION, download=False)
     for _ in range(3):
-        dev.sieve(lo, hi, N.TRIANGLE)
+        dev.sieve(lo, hi, N.TRIANGLE, shard=shard)
     ms = dev.timings_ms()["sieve"]
     buf = (C.c_ulonglong * (3 * 8192))()
     assert L.cgpu_debug_warp_clocks(buf, 8192) == 0
@@ -26,7 +28,7 @@ for name in sys.argv[1].split(","):
     t0 = a[:, 0].min()
     st, en, sm = (a[:, 0] - t0) / 1e3, (a[:, 1] - t0) / 1e3, a[:, 2]
     busy = en - st
-    print(f"{name}: kernel {ms * 1e3:.0f} us, warps {len(a)}; start max {st.max():.1f} us; "
+    print(f"{spec}: kernel {ms * 1e3:.0f} us, warps {len(a)}; start max {st.max():.1f} us; "
           f"end min/p10/p50/p90/max {np.percentile(en, [0, 10, 50, 90, 100]).round(1).tolist()}; "
           f"busy mean {busy.mean():.1f} std {busy.std():.1f}")
     sm_end = np.array([en[sm == s].max() for s in np.unique(sm)])
