@@ -108,7 +108,7 @@ constexpr uint32_t kPlanChunk = 1024;  // row slots per plan CTA
 // per row slot: nf | even << 8 | window-weight shift << 16, the odd factors,
 // then their Barrett constants
 constexpr uint32_t kFacWords = 1 + 2 * kMaxFactors;
-constexpr float kDefaultDrainAlpha = 8.0f;
+constexpr float kDefaultDrainAlpha = 12.0f;
 
 struct SieveArgs {
 	const uint32_t* ext;          // row-extended tables
