@@ -274,8 +274,8 @@ __device__ __forceinline__ uint32_t factorise_chunk(const SieveArgs& a, PlanSmem
 	float surv = 1.0f, cop = even ? 0.5f : 1.0f;
 	const uint32_t p32 = static_cast<uint32_t>(rb.p);
 	for (uint32_t j = 0; j < a.nreg; ++j)
-		if (p32 % a.reg_r[j]) surv *= 1.0f - sm.kill[j];
-	for (uint32_t j = 0; j < nf; ++j) cop *= 1.0f - 1.0f / static_cast<float>(out[1 + j]);
+		if (mod_full(p32, a.reg_r[j], a.reg_m[j])) surv *= 1.0f - sm.kill[j];
+	for (uint32_t j = 0; j < nf; ++j) cop -= cop * __frcp_rn(static_cast<float>(out[1 + j]));
 	const float wt = 1.0f + a.drain_alpha * (1.0f - __expf(-32.0f * cop * surv));
 	const uint32_t shift = wt >= 6.0f ? 3u : wt >= 3.0f ? 2u : wt >= 1.5f ? 1u : 0u;
 	out[0] |= shift << 16;
