@@ -280,6 +280,35 @@ def test_register_probe_layouts_vs_oracle(dev, case, monkeypatch):
         assert np.array_equal(r.survivor_pairs, o["survivor_pairs"])
 
 
+@pytest.mark.parametrize("row_cost,alpha", [("1", "0"), ("5000", "0"), ("800", "40"), ("50", "12")])
+def test_load_balance_knobs_never_change_results(golden, sets, row_cost, alpha, monkeypatch):
+    """The plan's work units (row setup charge, drain-aware window weights)
+    only move rows between warps: extreme settings give the reference's C3
+    result exactly, whole and as 3 block-cyclic shards."""
+    monkeypatch.setenv("CUBOID_ROW_COST", row_cost)
+    monkeypatch.setenv("CUBOID_DRAIN_ALPHA", alpha)
+    d = Device(0)  # knobs are read when a context is created
+    try:
+        P = sets["odd64"]
+        tb, _ = port.build_set(P)
+        d.load(P, tb)
+        g = golden["sieve"]["C3"]
+        want = {str(k): v for k, v in g["kill_histogram"].items()}
+        r = d.sieve(2, 10000, N.TRIANGLE)
+        assert (r.pairs_tested, r.survivors) == (g["pairs_tested"], g["survivors"])
+        assert {str(P[k]): int(c) for k, c in enumerate(r.hist) if c} == want
+        hist = np.zeros(len(P), np.uint64)
+        pairs = 0
+        for k in range(3):
+            x = d.sieve(2, 10000, N.TRIANGLE, shard=(3, k))
+            hist += x.hist
+            pairs += x.pairs_tested
+        assert pairs == g["pairs_tested"]
+        assert {str(P[k]): int(c) for k, c in enumerate(hist) if c} == want
+    finally:
+        d.close()
+
+
 def test_heavy_survivor_compaction(dev):
     """Weak sieve {11} (test_engine.cpp:177-197) over C1's triangle: 405,546
     survivors, emitted in canonical ascending (p, q) order."""
