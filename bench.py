@@ -350,6 +350,27 @@ def run_ours(args, wl, primes):
     tables, _ = dev.build(primes, N.BUILD_PRODUCTION)
     killable = dev.killable()
     n = len(primes)
+
+    # ---- per-rank compute of the N-GPU strong-scaling shapes, on this one GPU ------------
+    # (plan + sieve of every block-cyclic shard g of G; the slowest one against
+    # the whole launch / G -- what an N-rank run's compute can reach before its
+    # all-reduce; the collective itself needs N GPUs)
+    shard_scaling = None
+    if world == 1:
+        def best_total(shard, k=3):
+            t = []
+            for _ in range(k):
+                dev.sieve(wl["p_lo"], wl["p_hi"], N.TRIANGLE, shard=shard, surv_cap=1 << 16)
+                t.append(dev.timings_ms()["total"])
+            return min(t)
+        full_ms = best_total((1, 0))
+        shard_scaling = {"full_ms": full_ms,
+                         "note": "per-rank plan+sieve device time of block-cyclic shards on one GPU; "
+                                 "no collective, no L2 flush"}
+        for G in (2, 4, 8):
+            worst = max(best_total((G, g)) for g in range(G))
+            shard_scaling[str(G)] = {"slowest_shard_ms": worst, "ideal_ms": full_ms / G,
+                                     "efficiency": full_ms / G / worst}
     G, g = world, rank
     nblocks = wl["p_hi"] // 100 - wl["p_lo"] // 100 + 1
     # One int64 exchange buffer, reduced by ONE all-reduce(SUM) per step:
@@ -549,6 +570,7 @@ def run_ours(args, wl, primes):
             "table_build": table_build,
             "historical_region_scan": historical,
             "other_configs": other or None,
+            "strong_scaling_per_rank": shard_scaling,
             "clocks": clk.summary(),
         }
         if world == 1 and not args.no_cpu_baseline:
