@@ -269,13 +269,42 @@ def run_ours(args, wl, primes):
     # ---- table build (BASELINE config 2): exhaustive Z_r^3, 256 primes --------------
     from paper_1601_00636_b200.primes import odd_primes
     P256 = odd_primes(256)
+    # At N > 1 the primes are split over the ranks, balanced by r^3 (largest
+    # first onto the least-loaded rank); each rank builds its share and the
+    # job's rate is all evaluations over the slowest rank's build time.
+    loads = [0] * world
+    mine = []
+    for r in sorted(P256, reverse=True):
+        k = loads.index(min(loads))
+        loads[k] += r ** 3
+        if k == rank:
+            mine.append(r)
+    mine.sort()
     tb_ms = []
+    my_bytes = b""
     for i in range(3):
-        _, evals = dev.build(P256, N.BUILD_EXHAUSTIVE, download=False)
+        if mine:
+            my_bytes, evals = dev.build(mine, N.BUILD_EXHAUSTIVE, download=(i == 2))
         if i:
-            tb_ms.append(dev.timings_ms()["plan"])  # ms[0] = build kernels
-    cube_ms = float(np.mean(tb_ms))
+            tb_ms.append(dev.timings_ms()["plan"] if mine else 0.0)  # ms[0] = build kernels
+    cube_ms = allreduce_max(float(np.mean(tb_ms)))
     tb_evals = sum(r ** 3 for r in P256)
+    tb_parity = None
+    if world > 1:  # assemble the shares on every rank and compare with a whole production build
+        objs = [None] * world
+        dist.all_gather_object(objs, (mine, my_bytes))
+        full_prod, _ = dev.build(P256, N.BUILD_PRODUCTION)
+        offs, _ = Device.layout(P256)
+        pos = {r: int(o) for r, o in zip(P256, offs)}
+        ok = True
+        for primes_k, bytes_k in objs:
+            if not primes_k:
+                continue
+            offs_k, _ = Device.layout(primes_k)
+            for j, r in enumerate(primes_k):
+                nb = (r * r + 7) // 8
+                ok &= bytes_k[int(offs_k[j]):int(offs_k[j]) + nb] == full_prod[pos[r]:pos[r] + nb]
+        tb_parity = "ok" if ok else "MISMATCH"
     prod_t = []
     for i in range(3):
         dev.build(P256, N.BUILD_PRODUCTION, download=False)
@@ -286,6 +315,7 @@ def run_ours(args, wl, primes):
         "config": "C2: first 256 odd primes (3..1621), every (a,b,t) in Z_r^3, sum r^3 = "
                   f"{tb_evals} evals, 25,869,968 B of tables",
         "ms": cube_ms, "production_build_ms": float(np.mean(prod_t)),
+        "ranks": world, "sharded_parity": tb_parity,
         # k_cube_f2 evaluates A = c0 + c1 s + ... + c4 s^4 exactly in FP32 (balanced
         # residues, |A| < 2^22, on top of 1.5 * 2^23) with two (a,b) pairs per
         # FFMA2, then tests (A + s^5) for divisibility by r with one IMAD by
@@ -293,14 +323,14 @@ def run_ours(args, wl, primes):
         # The bound is that mix's measured throughput (cgpu_fp32_peak).
         "roofline": {"bound": "fp32_fma_pipes", "instr_per_eval": "2 FFMA2 + 1 IMAD + 1 VIMNMX",
                      "achieved": tb_evals / (cube_ms * 1e-3),
-                     "peak": fp_peak["cube_mix_evals"], "unit": "evals/s",
-                     "frac": tb_evals / (cube_ms * 1e-3) / fp_peak["cube_mix_evals"],
+                     "peak": fp_peak["cube_mix_evals"] * world, "unit": "evals/s",
+                     "frac": tb_evals / (cube_ms * 1e-3) / (fp_peak["cube_mix_evals"] * world),
                      "fp32_peaks": fp_peak,
                      # the same bound from the pipes alone: 2 FFMA2 + 1 IMAD per eval
                      # issued at their separately measured chain rates
                      "fma_pipe_model_evals": 1.0 / (2.0 / (fp_peak["ffma2_lane_fmas"] / 2)
                                                     + 1.0 / int_peak["fma_imad"]),
-                     "frac_vs_fma_pipe_model": tb_evals / (cube_ms * 1e-3) / (
+                     "frac_vs_fma_pipe_model": tb_evals / (cube_ms * 1e-3) / world / (
                          1.0 / (2.0 / (fp_peak["ffma2_lane_fmas"] / 2) + 1.0 / int_peak["fma_imad"])),
                      "imad_path_peak_evals": int_peak["fma_imad"] / 5,
                      "horner_ops_per_eval_survey": 27,
