@@ -272,14 +272,7 @@ def run_ours(args, wl, primes):
     # At N > 1 the primes are split over the ranks, balanced by r^3 (largest
     # first onto the least-loaded rank); each rank builds its share and the
     # job's rate is all evaluations over the slowest rank's build time.
-    loads = [0] * world
-    mine = []
-    for r in sorted(P256, reverse=True):
-        k = loads.index(min(loads))
-        loads[k] += r ** 3
-        if k == rank:
-            mine.append(r)
-    mine.sort()
+    mine = parallel.primes_by_cube(P256, world, rank)
     tb_ms = []
     my_bytes = b""
     for i in range(3):

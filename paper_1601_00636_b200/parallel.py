@@ -104,6 +104,21 @@ def gather_survivors(keys, count: int, group=None):
     return np.stack([allk >> np.uint64(32), allk & np.uint64(0xFFFFFFFF)], 1)
 
 
+def primes_by_cube(primes, G: int, g: int) -> list[int]:
+    """Rank g's share of an exhaustive table build (BASELINE C2) over G ranks:
+    primes dealt largest r^3 first onto the least-loaded rank (ties to the
+    lowest rank), returned ascending. Every prime lands on exactly one rank
+    and the largest load exceeds the mean by at most one table's r^3."""
+    loads = [0] * G
+    mine = []
+    for r in sorted(primes, reverse=True):
+        k = loads.index(min(loads))
+        loads[k] += r ** 3
+        if k == g:
+            mine.append(r)
+    return sorted(mine)
+
+
 def table_slice(total: int, G: int, g: int) -> tuple[int, int, int]:
     """Rank g's share of a G-way table upload: (lo, hi, chunk) with equal
     chunks of ceil(total / G) bytes (the last rank's slice may be short or

@@ -41,6 +41,17 @@ def test_partition_balances_triangle_work():
     assert max(work) / min(work) < 1.01
 
 
+def test_exhaustive_build_split_by_cube():
+    """The C2 build's prime split: a partition, balanced in r^3 to within the
+    largest single table."""
+    P = odd_primes(256)
+    for G in (1, 2, 3, 8):
+        parts = [parallel.primes_by_cube(P, G, g) for g in range(G)]
+        assert sorted(r for part in parts for r in part) == sorted(P)
+        loads = [sum(r ** 3 for r in part) for part in parts]
+        assert max(loads) - sum(loads) / G <= max(P) ** 3
+
+
 def test_table_slices_cover_the_set_once():
     for total in (0, 1, 7, 21873, 25869968):
         for G in (1, 2, 3, 8):
