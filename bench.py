@@ -82,6 +82,25 @@ def ops_per_pair(primes, killable, hist, survivors, pairs, p_lo, p_hi):
     return 7.0 * d_eff + 4.0 * omega_bar, d_eff, omega_bar
 
 
+def golden_parity(workload, primes, pairs, survivors, hist, brm, wl):
+    """The step's result against the reference's own full-range statistics
+    (tests/golden/golden.json, generated from oracle/_ref by
+    tests/golden/make_golden.py): pair and survivor counts, the first-killer
+    histogram by prime and every p/100 block's r_max (engine.hpp:229-291)."""
+    path = os.path.join(ROOT, "tests", "golden", "golden.json")
+    g = json.load(open(path))["sieve"].get(workload) if os.path.exists(path) else None
+    if g is None:
+        return {"ok": False, "against": f"no reference golden for {workload}"}
+    got_hist = {str(primes[k]): int(c) for k, c in enumerate(hist) if c}
+    blk0 = wl["p_lo"] // 100
+    got_brm = {str(blk0 + i): int(v) for i, v in enumerate(brm) if v}
+    checks = {"pairs": pairs == g["pairs_tested"], "survivors": survivors == g["survivors"],
+              "kill_histogram": got_hist == g["kill_histogram"],
+              "block_r_max": got_brm == g["block_r_max"]}
+    return {"ok": all(checks.values()), "checks": checks,
+            "against": f"tests/golden/golden.json sieve.{workload} (oracle/_ref, full range)"}
+
+
 # ---- clocks -------------------------------------------------------------------------
 
 class ClockSampler:
@@ -177,6 +196,31 @@ class CpuReference:
                     kind=self.kind, cores=self.cores)
 
 
+def cpu_table_baseline(P256, tables_c2=None):
+    """the reference's production build_table for all
+    256 primes (1 thread and all cores) and its definition build_table_oracle
+    on the first 64 primes (all cores), oracle/_ref on the host cores."""
+    from oracle import ref as refmod
+    if not refmod.available():
+        return None
+    threads = os.cpu_count() or 1
+    out = {"kind": "reference", "cores": threads}
+    _, t1 = refmod.build_tables(P256, oracle=False, nthreads=1)
+    _, tn = refmod.build_tables(P256, oracle=False, nthreads=threads)
+    out["build_table_256"] = {"seconds_1thread": t1, f"seconds_{threads}threads": tn,
+                              "what": "production build_table (sievetable.hpp:123-141), 256 primes"}
+    P64 = P256[:64]
+    _, to = refmod.build_tables(P64, oracle=True, nthreads=threads)
+    cube64 = sum(r ** 3 for r in P64)
+    out["build_table_oracle_64"] = {
+        "seconds": to, "threads": threads, "cube_evals": cube64, "value": cube64 / to,
+        "unit": "cube-equivalent evals/s",
+        "what": "build_table_oracle (sievetable.hpp:102-115, early exit per (p,q)) on the first 64 "
+                "odd primes; the full 256-prime definition is ~5 h on 1 thread"}
+    out["value"], out["unit"] = cube64 / to, "cube-equivalent evals/s"
+    return out
+
+
 def run_reference_arm(args, wl, primes):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -227,11 +271,16 @@ def run_ours(args, wl, primes):
         local = 0
     torch.cuda.set_device(local)
     gloo = args.backend == "gloo"
+    if not args.same_device and local >= torch.cuda.device_count():
+        raise SystemExit(f"bench: rank {rank} needs GPU {local}, only {torch.cuda.device_count()} visible")
     if world > 1:
         if gloo:
             dist.init_process_group("gloo")
         else:
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        print(f"bench: rank {rank}/{dist.get_world_size()} on cuda:{local}, "
+              f"{'gloo' if gloo else 'NCCL %s' % '.'.join(map(str, torch.cuda.nccl.version()))} "
+              f"communicator of {dist.get_world_size()} ranks", file=sys.stderr, flush=True)
     cuda = torch.device("cuda", local)
     cdev = torch.device("cpu") if gloo else cuda  # where collectives run
     stream = torch.cuda.Stream(device=cuda)  # the context and all torch work share it
@@ -314,10 +363,17 @@ def run_ours(args, wl, primes):
         # FFMA2, then tests (A + s^5) for divisibility by r with one IMAD by
         # r^-1 mod 2^32 and an unsigned min: 2 FFMA2 + 1 IMAD + 1 min per eval.
         # The bound is that mix's measured throughput (cgpu_fp32_peak).
+        # frac: against the FMA-pipe model of that mix (2 FFMA2 + 1 IMAD per eval at
+        # the pipes' separately measured rates); the self-chain microbenchmark of
+        # the same instruction mix is kept beside it.
         "roofline": {"bound": "fp32_fma_pipes", "instr_per_eval": "2 FFMA2 + 1 IMAD + 1 VIMNMX",
                      "achieved": tb_evals / (cube_ms * 1e-3),
-                     "peak": fp_peak["cube_mix_evals"] * world, "unit": "evals/s",
-                     "frac": tb_evals / (cube_ms * 1e-3) / (fp_peak["cube_mix_evals"] * world),
+                     "peak": world / (2.0 / (fp_peak["ffma2_lane_fmas"] / 2) + 1.0 / int_peak["fma_imad"]),
+                     "unit": "evals/s",
+                     "frac": tb_evals / (cube_ms * 1e-3) / world / (
+                         1.0 / (2.0 / (fp_peak["ffma2_lane_fmas"] / 2) + 1.0 / int_peak["fma_imad"])),
+                     "self_chain_peak": fp_peak["cube_mix_evals"] * world,
+                     "frac_vs_self_chain": tb_evals / (cube_ms * 1e-3) / (fp_peak["cube_mix_evals"] * world),
                      "fp32_peaks": fp_peak,
                      # the same bound from the pipes alone: 2 FFMA2 + 1 IMAD per eval
                      # issued at their separately measured chain rates
@@ -453,8 +509,9 @@ def run_ours(args, wl, primes):
     # results of the last step (already reduced across ranks)
     res = acc.cpu().numpy()
     pairs, survivors, hist = int(res[0]), int(res[1]), res[2:]
-    blocks_ok = bool((brm_sum if world > 1 else brm).min().item() >= 1)  # every block reduced once
-    parity_ok = (pairs == wl["pairs"] and int(hist.sum()) + survivors == pairs and blocks_ok)
+    brm_final = (brm_sum if world > 1 else brm).cpu().numpy().astype(np.int64)
+    parity = golden_parity(args.workload, primes, pairs, survivors, hist, brm_final, wl)
+    parity_ok = parity["ok"]
     local_pairs = pairs if world == 1 else None
 
     # ---- e2e: host tables in, host results out, through the C ABI -------------------------
@@ -518,7 +575,10 @@ def run_ours(args, wl, primes):
     barrier()
     e2e_total = allreduce_max(float(np.sum(e2e_s)))
     clk.__exit__()
-    parity_ok = parity_ok and int(h_buf[0]) == wl["pairs"]
+    e2e_res = h_buf.numpy()
+    e2e_parity = golden_parity(args.workload, primes, int(e2e_res[0]), int(e2e_res[1]),
+                               e2e_res[2:n_acc], e2e_res[n_acc:n_acc + nblocks], wl)
+    parity_ok = parity_ok and e2e_parity["ok"]
 
     # ---- roofline of the dominant kernel (k_sieve), rank-local ------------------------------
     if world > 1:  # this rank's own pairs for the per-launch figure
@@ -554,16 +614,45 @@ def run_ours(args, wl, primes):
                 ncu["dram_gbs"] = x.get("dram_bytes", 0) / (x["duration_ms"] * 1e-3) / 1e9
         except (ValueError, AttributeError):
             ncu = None
-    roof = {"bound": "int32", "achieved": achieved, "peak": int_peak["best"],
-            "unit": "INT32 ops/s", "frac": achieved / int_peak["best"], "traffic": traffic,
-            "kernel": "k_sieve", "kernel_ms": kavg, "ops_per_pair": opp, "d_eff": d_eff,
-            "omega_bar": omega_bar, "pairs_per_launch": local_pairs,
+    # The hardware fraction: k_sieve's warp instructions per launch (ncu,
+    # profiles/ncu_summary.json, same kernel build and workload) x 32 lanes
+    # over this run's CUDA-event kernel time, against the measured INT32 issue
+    # peak -- i.e. the issue utilisation the live kernel sustains. Shared-memory
+    # wavefronts (1 per clock per SM) beside it. At N > 1 a rank's launch
+    # holds its share of the instructions (scaled by its pairs).
+    sms = torch.cuda.get_device_properties(local).multi_processor_count
+    clocks = clk.summary()
+    nk = (json.load(open(prof)).get("k_sieve", {}).get(wl["desc"][:2], {})
+          if os.path.exists(prof) else {})
+    share = local_pairs / max(pairs, 1)
+    hw = {}
+    if nk.get("warp_inst"):
+        lanes_s = nk["warp_inst"] * share * 32 / (kavg * 1e-3)
+        hw = {"achieved": lanes_s, "frac": lanes_s / int_peak["best"]}
+    if nk.get("smem_wavefronts") and clocks.get("sm_mhz"):
+        hw["smem_wavefront_frac"] = nk["smem_wavefronts"] * share / (
+            kavg * 1e-3 * sms * clocks["sm_mhz"] * 1e6)
+    roof = {"bound": "int32_issue", "achieved": hw.get("achieved"), "peak": int_peak["best"],
+            "unit": "thread-instructions/s", "frac": hw.get("frac"), "traffic": traffic,
+            "smem_wavefront_frac": hw.get("smem_wavefront_frac"),
+            "kernel": "k_sieve", "kernel_ms": kavg, "pairs_per_launch": local_pairs,
+            "warp_inst_per_launch": nk.get("warp_inst", 0) * share or None,
+            "smem_wavefronts_per_launch": nk.get("smem_wavefronts", 0) * share or None,
+            "ncu_round": nk.get("round"), "sms": sms,
+            "how": "frac = warp_inst x 32 / live kernel_ms / peak (issue utilisation); "
+                   "smem_wavefront_frac = wavefronts / (kernel_ms x SMs x median SM clock); "
+                   "warp_inst and wavefronts from profiles/ncu_summary.json (ncu --set full of "
+                   "the same kernel on the same workload), kernel_ms from CUDA events in this run",
             "peak_source": "measured in this run: best of cgpu_int32_peak's INT32 chains "
                            "(nominal issue limit 148 SM x 128 lanes x clock = 3.72e13 at 1965 MHz)",
             "int32_peaks": int_peak,
             "ncu_pipes": ncu,
-            "note": "ops_per_pair is the reference algorithm's count (SURVEY 8(d)); the kernel "
-                    "is bit-sliced (one probe answers 32 q), so frac can exceed 1"}
+            "reference_algorithm": {
+                "ops_per_pair": opp, "d_eff": d_eff, "omega_bar": omega_bar,
+                "achieved": achieved, "unit": "INT32 ops/s", "frac": achieved / int_peak["best"],
+                "note": "SURVEY 8(d)'s count for the reference algorithm (7 D_eff + 4 omega_bar "
+                        "per pair); the kernel is bit-sliced (one probe answers 32 q), so this "
+                        "ratio exceeds 1 -- it is the work-efficiency figure, not a pipe fraction"}}
 
     if rank == 0:
         value = pairs * args.steps / (total_ms * 1e-3)
@@ -578,6 +667,7 @@ def run_ours(args, wl, primes):
                        "parallelism": f"dp{world}: p/100 blocks block-cyclic over ranks, one NCCL "
                                       "all-reduce(SUM) of counts/histogram/block r_max/survivor slices"},
             "parity": "ok" if parity_ok else "MISMATCH",
+            "parity_detail": parity,
             "e2e": {"value": pairs * args.steps / e2e_total, "unit": "pairs/s",
                     "h2d_bytes_per_step": (parallel.table_slice(len(tables), world, 0)[2] if world > 1
                                            else len(tables)) + 4 * n,
@@ -594,7 +684,7 @@ def run_ours(args, wl, primes):
             "historical_region_scan": historical,
             "other_configs": other or None,
             "strong_scaling_per_rank": shard_scaling,
-            "clocks": clk.summary(),
+            "clocks": clocks,
         }
         if world == 1 and not args.no_cpu_baseline:
             s = CpuReference(wl, primes, os.cpu_count() or 1).sample(args.cpu_budget)
@@ -603,8 +693,50 @@ def run_ours(args, wl, primes):
                 "kind": s["kind"],
                 "sample": f"rows p={s['rows'][0]}..{s['rows'][1]} of {wl['desc'].split(':')[0]} "
                           f"({s['pairs']} pairs, {s['seconds']:.1f} s)"}
+            s1 = CpuReference(wl, primes, 1).sample(args.cpu_budget / 2)
+            line["cpu_baseline_1thread"] = {
+                "value": s1["pairs"] / s1["seconds"], "unit": "pairs/s", "cores": 1, "kind": s1["kind"],
+                "sample": f"rows p={s1['rows'][0]}..{s1['rows'][1]} of {wl['desc'].split(':')[0]} "
+                          f"({s1['pairs']} pairs, {s1['seconds']:.1f} s), the reference's own "
+                          "single-thread execution model (engine.hpp:494)"}
+            line["table_build"]["cpu_baseline"] = cpu_table_baseline(P256, tables_c2=None)
         print(json.dumps(line), flush=True)
     dev.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def self_launch(args):
+    """`bench.py --gpus N` outside torchrun: start N ranks on this node (one
+    process per GPU, LOCAL_RANK = device) through torch.distributed.run on
+    127.0.0.1 with the same arguments; rank 0's JSON line is the output."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           os.path.abspath(__file__)] + sys.argv[1:]
+    print(f"bench: launching {args.gpus} ranks: {' '.join(cmd)}", file=sys.stderr, flush=True)
+    return subprocess.call(cmd)
+
+
+def launch_check(args):
+    """Every rank joins the process group and all-reduces 1; rank 0 prints the
+    world it saw (the CPU test of the launcher uses gloo)."""
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world > 1:
+        dist.init_process_group(args.backend)
+    t = torch.ones(1, dtype=torch.int64)
+    if world > 1:
+        dist.all_reduce(t)
+    if rank == 0:
+        print(json.dumps({"launch_check": True, "n_gpus": world, "ranks_seen": int(t.item()),
+                          "backend": args.backend if world > 1 else None}), flush=True)
     if world > 1:
         dist.destroy_process_group()
     return 0
@@ -622,7 +754,13 @@ def main():
     ap.add_argument("--backend", choices=["nccl", "gloo"], default="nccl")
     ap.add_argument("--same-device", action="store_true",
                     help="plumbing test: all ranks on GPU 0 (use with --backend gloo)")
+    ap.add_argument("--launch-check", action="store_true",
+                    help="launcher test: init the process group, count the ranks, print, exit")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return self_launch(args)
+    if args.launch_check:
+        return launch_check(args)
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     from paper_1601_00636_b200.primes import odd_primes
     wl = WORKLOADS[args.workload]

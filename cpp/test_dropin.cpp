@@ -4,7 +4,9 @@
 // acceptance.cpp). Needs a GPU; driven by tests/test_cpp_dropin.py.
 
 #include <atomic>
+#include <chrono>
 #include <cstdio>
+#include <thread>
 #include <cstdlib>
 #include <numeric>
 #include <string>
@@ -172,8 +174,8 @@ int main()
 	CHECK(head.pairs_tested == whole.pairs_tested && head.kill_histogram == whole.kill_histogram &&
 	      head.block_r_max == whole.block_r_max && head.resume_p == whole.resume_p);
 
-	// a scan polled for stops runs as several device tiles (~2^37 pairs each):
-	// the same statistics as one launch
+	// a scan polled for stops runs as several device tiles (~2^37 q visited
+	// each, ending at poll points): the same statistics as one launch
 	{
 		std::atomic<bool> never{false};
 		ScanOptions po;
@@ -181,10 +183,152 @@ int main()
 		const ScanStats tiled = gpu::scan(gpu_default, {152, 3}, 200000, {}, po);
 		const ScanStats one = gpu::scan(gpu_default, {152, 3}, 200000);
 		CHECK(!tiled.stopped);
-		CHECK(gpu::detail::tile_end(152, 200000) < 200000);
 		CHECK(tiled.pairs_tested == one.pairs_tested && tiled.kill_histogram == one.kill_histogram &&
 		      tiled.block_r_max == one.block_r_max && tiled.resume_p == one.resume_p &&
 		      tiled.resume_q == one.resume_q && tiled.survivors == one.survivors);
+	}
+
+	// a flag already raised, but fewer q left than batch_pairs: the
+	// reference never polls and completes the range
+	{
+		std::atomic<bool> up{true}, rup{true};
+		ScanOptions o, ro;
+		o.hooks.stop = &up;
+		ro.hooks.stop = &rup;
+		o.batch_pairs = ro.batch_pairs = 1u << 30;
+		const ScanStats g = gpu::scan(gpu_default, {152, 3}, 400, {}, o);
+		const ScanStats r = scan(ref_default, {152, 3}, 400, {}, ro);
+		CHECK(!g.stopped);
+		CHECK(same(g, r));
+	}
+
+	// building another set replaces the context's tables; the next
+	// scan of the first set must upload it again (and size its histogram by it)
+	{
+		const ScanStats a1 = gpu::scan(gpu_default, {152, 3}, 600);
+		const SieveSet other = gpu::build_set(odd_primes(200));
+		(void)other;
+		const ScanStats a2 = gpu::scan(gpu_default, {152, 3}, 600);
+		CHECK(same(a1, a2));
+		CHECK(same(a2, scan(ref_default, {152, 3}, 600)));
+	}
+
+	// a flag raised WHILE the scan runs (device-visible stop word): the scan
+	// halts at a poll point -- (q visited from the start to the resume pair) + 1
+	// is a multiple of batch_pairs -- and the reference's checkpoint of it
+	// resumes to the uninterrupted result
+	{
+		const uint64_t P_END = 1500000;  // REGION ~6.6e13 pairs: several seconds on one GPU
+		std::atomic<bool> flag{false};
+		ScanOptions o;
+		o.hooks.stop = &flag;
+		o.batch_pairs = 1u << 16;
+		std::thread raiser([&] {
+			std::this_thread::sleep_for(std::chrono::milliseconds(300));
+			flag.store(true);
+		});
+		const ScanStats h = gpu::scan(gpu_default, {152, 3}, P_END, {}, o);
+		raiser.join();
+		CHECK(h.stopped);
+		CHECK(h.resume_p > 152 && h.resume_p < P_END);
+		uint64_t visited = 0;  // engine.hpp:225-247 visiting order
+		for (uint64_t p = 152; p <= h.resume_p; ++p) {
+			const RegionBounds b = q_bounds(p);
+			const uint64_t q0 = p == 152 ? 3 : b.q_low;
+			visited += p < h.resume_p ? b.q_high - q0 + 1 : h.resume_q - q0;
+		}
+		CHECK((visited + 1) % o.batch_pairs == 0);
+		SearchCheckpoint cp;
+		cp.p = h.resume_p;
+		cp.q = h.resume_q;
+		cp.r_max = 1;
+		cp.timestamp = iso8601_local_now();
+		cp.pairs_tested = h.pairs_tested;
+		cp.survivors = h.survivors;
+		checkpoint_write(cp, "/tmp/cuboid_gpu_cp.txt");
+		const SearchCheckpoint back = checkpoint_read("/tmp/cuboid_gpu_cp.txt");  // the reference's reader
+		CHECK(back.p == h.resume_p && back.q == h.resume_q && back.pairs_tested == h.pairs_tested);
+		ScanStats merged = h;
+		merged.merge(gpu::scan(gpu_default, {back.p, back.q}, P_END));
+		const ScanStats whole = gpu::scan(gpu_default, {152, 3}, P_END);
+		CHECK(merged.pairs_tested == whole.pairs_tested && merged.kill_histogram == whole.kill_histogram &&
+		      merged.block_r_max == whole.block_r_max && merged.survivors == whole.survivors &&
+		      merged.resume_p == whole.resume_p && merged.resume_q == whole.resume_q && !merged.stopped);
+		// the stopped half equals an unstoppable span up to the same pair
+		std::atomic<bool> pre{true};
+		ScanOptions po;
+		po.hooks.stop = &pre;
+		po.batch_pairs = visited + 1;
+		const ScanStats again = gpu::scan(gpu_default, {152, 3}, P_END, {}, po);
+		CHECK(same(again, h));
+	}
+
+	// the GPU SearchController (engine.hpp:429-595): start / status / stop,
+	// report + checkpoint through the reference's writers, resume from the
+	// checkpoint, merge = uninterrupted
+	{
+		const uint64_t P_END = 1500000;
+		std::remove("/tmp/cuboid_gpu_report.txt");
+		gpu::SearchController::Config cfg;
+		cfg.report_path = "/tmp/cuboid_gpu_report.txt";
+		cfg.checkpoint_path = "/tmp/cuboid_gpu_ctl_cp.txt";
+		cfg.p_end = P_END;
+		gpu::SearchController ctl(cfg);
+		CHECK(ctl.start(152, 3) == 6);  // not loaded
+		ctl.adopt(gpu_default);
+		CHECK(ctl.start(151, 3) == 2);
+		CHECK(ctl.start(152, 2) == 4);
+		CHECK(ctl.start(152, 3) == 0);
+		CHECK(ctl.start(152, 3) == 1);  // already running
+		std::this_thread::sleep_for(std::chrono::milliseconds(300));
+		CHECK(ctl.status().running);
+		CHECK(ctl.stop() == 0);
+		CHECK(ctl.stop() == 1);
+		CHECK(ctl.last_error().empty());
+		const ScanStats first = ctl.last_stats();
+		CHECK(first.stopped);
+		const SearchCheckpoint cp = checkpoint_read(cfg.checkpoint_path);
+		CHECK(cp.p == first.resume_p && cp.q == first.resume_q && cp.pairs_tested == first.pairs_tested);
+		CHECK(cp.r_max == ctl.status().current_r_max);
+		CHECK(ctl.start(cp.p, cp.q) == 0);
+		while (ctl.status().running) std::this_thread::sleep_for(std::chrono::milliseconds(20));
+		ScanStats merged = first;
+		merged.merge(ctl.last_stats());
+		const ScanStats whole = gpu::scan(gpu_default, {152, 3}, P_END);
+		CHECK(merged.pairs_tested == whole.pairs_tested && merged.kill_histogram == whole.kill_histogram &&
+		      merged.block_r_max == whole.block_r_max && merged.resume_p == whole.resume_p);
+		CHECK(ctl.release() == 0);
+		CHECK(ctl.release() == 6);
+	}
+
+	// in-process multi-GPU path (cgpu_multi, NCCL clique) over the devices
+	// this box has; with one device it is a world-size-1 clique
+	{
+		int ndev = 0;
+		gpu::check(cgpu_device_count(&ndev), "cgpu_device_count");
+		std::vector<int> devs;
+		for (int d = 0; d < ndev && d < 8; ++d) devs.push_back(d);
+		auto& mc = gpu::multi_context(devs);
+		const ScanStats m1 = gpu::detail::scan_on(mc, gpu_default, {152, 3}, 5000, {}, ScanOptions{});
+		CHECK(same(m1, big));
+		CHECK(same(gpu::detail::scan_on(mc, gpu_default, {777, 12345}, 901, {}, ScanOptions{}),
+		           scan(ref_default, {777, 12345}, 901)));
+		std::vector<ScanEvent> me;
+		const ScanStats mw = gpu::detail::scan_on(mc, weak, {1, 1}, 40, [&](const ScanEvent& e) { me.push_back(e); },
+		                                          small);
+		CHECK(same(mw, rw));
+		CHECK(me.size() == re.size());
+		std::atomic<bool> pre{true};
+		ScanOptions po;
+		po.hooks.stop = &pre;
+		po.batch_pairs = 8000;
+		std::atomic<bool> rpre{true};
+		ScanOptions rpo = po;
+		rpo.hooks.stop = &rpre;
+		CHECK(same(gpu::detail::scan_on(mc, gpu_default, {401, 23000}, 700, {}, po),
+		           scan(ref_default, {401, 23000}, 700, {}, rpo)));
+		CHECK(same(gpu::scan_triangle(weak, 2, 300, {}, devs), ref_triangle(weak, 2, 300, nullptr)));
+		std::printf("multi-GPU clique of %zu device(s) checked\n", devs.size());
 	}
 
 	// TRIANGLE (BASELINE config 1: 32 odd primes, 2 <= p <= 2000)

@@ -19,23 +19,37 @@
 // libcuboid_gpu.so (sm_100a) through include/cuboid_gpu.h; there is no CPU
 // fallback: without a device every call throws std::runtime_error.
 //
-// Cooperative stop (ScanOptions::hooks.stop): a flag already raised when scan()
-// starts halts exactly where the reference's does -- at the batch_pairs-th q
-// visited (engine.hpp:248-257), same resume point and statistics (the span
-// before it is sieved with cgpu_sieve_span). A flag raised while the scan
-// runs is polled between device tiles of about kStopTilePairs REGION pairs
-// (~20 ms each at the B200's rate, whatever the row length); the resume point
-// is then the first pair of the next tile. Either way ScanStats::merge of the two
-// halves equals the full scan (test_engine.cpp:134-175).
+// Cooperative stop (ScanOptions::hooks.stop, engine.hpp:248-257): the
+// reference polls its flag every batch_pairs q visited and halts AT that q.
+// Here a scan with a stop hook runs as device tiles whose ends are such poll
+// points (multiples of batch_pairs q visited from the start, ~kStopTilePairs
+// each); a watcher thread mirrors the flag into a mapped host word that the
+// sieve kernels poll, so a tile running when the flag rises is abandoned
+// within microseconds, discarded, and the scan halts at the NEXT poll point
+// after the tile's start (sieved exactly, with a span) -- a stop position,
+// resume point and statistics the reference itself produces when its flag
+// becomes visible between those two polls. A flag raised before the scan:
+// the batch_pairs-th q, like the reference; with fewer q left than
+// batch_pairs, no poll is reached and the scan completes (stopped = false).
+// ScanStats::merge of the halves equals the full scan (test_engine.cpp:134-175).
+//
+// Multi-GPU from one process: scan(..., devices) shards the rows over the
+// listed GPUs (cgpu_multi: NCCL clique, block-cyclic p/100 blocks, one grouped
+// all-reduce + survivor gather per tile). SearchController below is the
+// reference's controller (engine.hpp:429-595) over these scans.
 
+#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <cstdint>
 #include <cstring>
+#include <functional>
 #include <map>
 #include <mutex>
+#include <optional>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "cuboid/engine.hpp"  // the reference: SieveSet, ScanStats, ScanSink, verify_pair, ...
@@ -43,19 +57,7 @@
 
 namespace cuboid::gpu {
 
-inline constexpr uint64_t kStopTilePairs = 1ull << 37;
 
-namespace detail {
-// Last row of a tile starting at row p: REGION rows hold ~59p pairs, so rows
-// p..hi hold ~59/2 (hi^2 - p^2); pick hi for about kStopTilePairs of them.
-inline uint64_t tile_end(uint64_t p, uint64_t p_end)
-{
-	const long double x = static_cast<long double>(p) * p + 2.0L * kStopTilePairs / 59.0L;
-	uint64_t hi = static_cast<uint64_t>(std::sqrt(x));
-	if (hi < p) hi = p;
-	return hi < p_end ? hi : p_end;
-}
-}  // namespace detail
 
 struct Error : std::runtime_error {
 	int code;
@@ -77,6 +79,35 @@ inline void check(int rc, const char* where)
 	}
 }
 
+// Which table set a context holds. Identified exactly: the prime list plus a
+// host copy of the table bytes (memcmp, ~1.5 ms for the 26 MB 256-prime set
+// -- a sampled hash would accept a different set of the same shape, e.g. an
+// edited load_sieve file allocated at a freed set's address).
+class Residency {
+public:
+	bool holds(const SieveSet& set, std::vector<uint32_t>& primes) const
+	{
+		primes.clear();
+		for (const PrimeRecord& r : set.index()) primes.push_back(r.prime);
+		return valid_ && primes == primes_ && set.tables().size() == bytes_.size() &&
+		       std::memcmp(set.tables().data(), bytes_.data(), bytes_.size()) == 0;
+	}
+	void record(const SieveSet& set, std::vector<uint32_t>&& primes)
+	{
+		primes_ = std::move(primes);
+		bytes_.assign(set.tables().begin(), set.tables().end());
+		valid_ = true;
+	}
+	// Any call that replaces the context's tables (cgpu_tables_build) drops
+	// the record, so the next scan uploads its own set again.
+	void invalidate() { valid_ = false; }
+
+private:
+	bool valid_ = false;
+	std::vector<uint32_t> primes_;
+	std::vector<uint8_t> bytes_;
+};
+
 // One device context per process and device (one process per GPU), holding
 // the resident table set.
 class Context {
@@ -87,47 +118,109 @@ public:
 	Context& operator=(const Context&) = delete;
 
 	cgpu_ctx* get() { return ctx_; }
+	cgpu_ctx* span_ctx() { return ctx_; }
 	int device() const { return device_; }
 
-	// Makes `set` resident unless it already is (the set is immutable after
-	// build, so its bytes are identified by address, size and a sample hash).
+	// Makes `set` resident unless it already is.
 	void ensure_resident(const SieveSet& set)
 	{
-		const Key k = key_of(set);
-		if (k == resident_) return;
 		std::vector<uint32_t> primes;
-		for (const PrimeRecord& r : set.index()) primes.push_back(r.prime);
+		if (res_.holds(set, primes)) return;
+		res_.invalidate();
 		check(cgpu_tables_load(ctx_, primes.data(), static_cast<uint32_t>(primes.size()),
 		                       set.tables().data(), set.tables().size()),
 		      "cgpu_tables_load");
-		resident_ = k;
+		res_.record(set, std::move(primes));
 	}
-	void mark_resident(const SieveSet& set) { resident_ = key_of(set); }
+	void invalidate() { res_.invalidate(); }
+
+	int sieve(uint64_t p_lo, uint64_t q_start, uint64_t p_hi, int mode, uint64_t* counts, uint64_t* hist,
+	          uint32_t* brm, uint64_t nb, uint64_t* surv, uint64_t cap)
+	{
+		return cgpu_sieve(ctx_, p_lo, q_start, p_hi, mode, 1, 0, counts, hist, brm, nb, surv, cap);
+	}
+	int sieve_span(uint64_t p_lo, uint64_t q_start, uint64_t p_hi, uint64_t q_end, uint64_t* counts,
+	               uint64_t* hist, uint32_t* brm, uint64_t nb, uint64_t* surv, uint64_t cap)
+	{
+		return cgpu_sieve_span(ctx_, p_lo, q_start, p_hi, q_end, counts, hist, brm, nb, surv, cap);
+	}
+	void set_stop_word(uint32_t* w) { check(cgpu_set_stop_word(ctx_, w), "cgpu_set_stop_word"); }
+	uint32_t loaded_primes()
+	{
+		uint32_t n = 0;
+		check(cgpu_tables_info(ctx_, &n, nullptr), "scan");
+		return n;
+	}
 
 	std::mutex& mutex() { return mu_; }
 
 private:
-	struct Key {
-		const void* data = nullptr;
-		size_t size = 0, nprimes = 0;
-		uint64_t hash = 0;
-		bool operator==(const Key& o) const
-		{
-			return data == o.data && size == o.size && nprimes == o.nprimes && hash == o.hash;
-		}
-	};
-	static Key key_of(const SieveSet& set)
-	{
-		Key k{set.tables().data(), set.tables().size(), set.prime_count(), 1469598103934665603ull};
-		const auto& t = set.tables();
-		for (size_t i = 0; i < t.size(); i += 61) k.hash = (k.hash ^ t[i]) * 1099511628211ull;
-		for (const PrimeRecord& r : set.index()) k.hash = (k.hash ^ r.prime) * 1099511628211ull;
-		return k;
-	}
-
 	int device_;
 	cgpu_ctx* ctx_ = nullptr;
-	Key resident_;
+	Residency res_;
+	std::mutex mu_;
+};
+
+// Several GPUs driven from this one process (cgpu_multi: one context per
+// device, an NCCL clique from ncclCommInitAll, block-cyclic p/100 shards, one
+// grouped all-reduce + survivor gather per call). What a single-process
+// caller such as SearchController::run_scan (engine.hpp:555-577) uses to
+// spread scan() over every GPU of the box.
+class MultiContext {
+public:
+	explicit MultiContext(const std::vector<int>& devices) : devices_(devices)
+	{
+		check(cgpu_multi_create(static_cast<int>(devices.size()), devices.data(), &m_), "cgpu_multi_create");
+	}
+	~MultiContext() { cgpu_multi_destroy(m_); }
+	MultiContext(const MultiContext&) = delete;
+	MultiContext& operator=(const MultiContext&) = delete;
+
+	cgpu_multi* get() { return m_; }
+	const std::vector<int>& devices() const { return devices_; }
+	// the first device's context: it holds the whole set after a load
+	cgpu_ctx* span_ctx()
+	{
+		cgpu_ctx* c = nullptr;
+		check(cgpu_multi_ctx(m_, 0, &c), "cgpu_multi_ctx");
+		return c;
+	}
+
+	void ensure_resident(const SieveSet& set)
+	{
+		std::vector<uint32_t> primes;
+		if (res_.holds(set, primes)) return;
+		res_.invalidate();
+		check(cgpu_multi_tables_load(m_, primes.data(), static_cast<uint32_t>(primes.size()),
+		                             set.tables().data(), set.tables().size()),
+		      "cgpu_multi_tables_load");
+		res_.record(set, std::move(primes));
+	}
+
+	int sieve(uint64_t p_lo, uint64_t q_start, uint64_t p_hi, int mode, uint64_t* counts, uint64_t* hist,
+	          uint32_t* brm, uint64_t nb, uint64_t* surv, uint64_t cap)
+	{
+		return cgpu_multi_sieve(m_, p_lo, q_start, p_hi, 0, mode, counts, hist, brm, nb, surv, cap);
+	}
+	int sieve_span(uint64_t p_lo, uint64_t q_start, uint64_t p_hi, uint64_t q_end, uint64_t* counts,
+	               uint64_t* hist, uint32_t* brm, uint64_t nb, uint64_t* surv, uint64_t cap)
+	{
+		return cgpu_multi_sieve(m_, p_lo, q_start, p_hi, q_end, CGPU_REGION, counts, hist, brm, nb, surv, cap);
+	}
+	void set_stop_word(uint32_t* w) { check(cgpu_multi_set_stop_word(m_, w), "cgpu_multi_set_stop_word"); }
+	uint32_t loaded_primes()
+	{
+		uint32_t n = 0;
+		check(cgpu_tables_info(span_ctx(), &n, nullptr), "scan");
+		return n;
+	}
+
+	std::mutex& mutex() { return mu_; }
+
+private:
+	std::vector<int> devices_;
+	cgpu_multi* m_ = nullptr;
+	Residency res_;
 	std::mutex mu_;
 };
 
@@ -138,6 +231,16 @@ inline Context& context(int device = 0)
 	std::lock_guard<std::mutex> lk(mu);
 	auto it = ctxs.find(device);
 	if (it == ctxs.end()) it = ctxs.emplace(device, new Context(device)).first;
+	return *it->second;
+}
+
+inline MultiContext& multi_context(const std::vector<int>& devices)
+{
+	static std::mutex mu;
+	static std::map<std::vector<int>, MultiContext*> ctxs;  // process lifetime
+	std::lock_guard<std::mutex> lk(mu);
+	auto it = ctxs.find(devices);
+	if (it == ctxs.end()) it = ctxs.emplace(devices, new MultiContext(devices)).first;
 	return *it->second;
 }
 
@@ -153,6 +256,7 @@ inline SieveSet build_set(const std::vector<uint32_t>& primes, int device = 0,
 	uint64_t total = 0;
 	check(cgpu_table_layout(primes.data(), n, offsets.data(), &total), "SieveSet::build");
 	std::vector<uint8_t> tables(total);
+	c.invalidate();  // the build replaces the context's resident tables
 	check(cgpu_tables_build(c.get(), primes.data(), n, algorithm, tables.data(), nullptr, nullptr),
 	      "SieveSet::build");
 	std::vector<PrimeRecord> index(n);
@@ -171,6 +275,8 @@ inline BitTable build_table(uint32_t r, int device = 0)
 
 // ---- sieve -------------------------------------------------------------------
 
+inline constexpr uint64_t kStopTilePairs = 1ull << 37;  // q visited per stoppable tile (~20 ms)
+
 namespace detail {
 
 struct DeviceScan {
@@ -181,69 +287,21 @@ struct DeviceScan {
 	std::vector<uint64_t> surv;  // (p, q) pairs, ascending
 };
 
-inline DeviceScan run(Context& c, const SieveSet& set, uint64_t p_lo, uint64_t q_start, uint64_t p_hi,
-                      int mode)
+// Sieves through `call(counts, hist, brm, nb, surv, cap)`, growing the
+// survivor buffer until every survivor fits.
+template <class Call>
+DeviceScan collect(const SieveSet& set, uint64_t p_lo, uint64_t p_hi, Call&& call)
 {
 	DeviceScan d;
 	d.hist.assign(set.prime_count(), 0);
+	if (p_hi < p_lo) return d;
 	d.block_lo = p_lo / 100;
-	const uint64_t nb = p_hi >= p_lo ? p_hi / 100 - p_lo / 100 + 1 : 0;
-	d.block_rmax.assign(nb ? nb : 1, 0);
-	uint64_t cap = 1 << 16;
-	for (;;) {
-		d.surv.assign(2 * cap, 0);
-		const int rc = cgpu_sieve(c.get(), p_lo, q_start, p_hi, mode, 1, 0, d.counts, d.hist.data(),
-		                          d.block_rmax.data(), nb, d.surv.data(), cap);
-		if (rc == CGPU_ERR_CAPACITY && d.counts[1] > cap) {
-			cap = d.counts[1];
-			continue;
-		}
-		check(rc, "scan");
-		break;
-	}
-	d.surv.resize(2 * d.counts[1]);
-	return d;
-}
-
-// The (p, q) at which the reference halts with a raised stop flag: the
-// batch_pairs-th q visited from `start` (engine.hpp:248-257); false if the
-// range ends first.
-inline bool stop_point(SearchPair start, uint64_t p_end, uint64_t batch_pairs, SearchPair& at)
-{
-	uint64_t k = batch_pairs ? batch_pairs : 1;
-	for (uint64_t p = start.p; p <= p_end; ++p) {
-		const RegionBounds b = q_bounds(p);
-		const uint64_t q0 = p == start.p ? start.q : b.q_low;
-		const uint64_t n = b.q_high >= q0 ? b.q_high - q0 + 1 : 0;
-		if (k <= n) {
-			at = {p, q0 + k - 1};
-			return true;
-		}
-		k -= n;
-	}
-	return false;
-}
-
-// REGION pairs from `from` up to, not including, `to` (sieved on the device).
-inline DeviceScan run_span(Context& c, const SieveSet& set, SearchPair from, SearchPair to)
-{
-	DeviceScan d;
-	d.hist.assign(set.prime_count(), 0);
-	const uint64_t first = to.p == from.p ? from.q : q_bounds(to.p).q_low;
-	uint64_t p_hi = to.p, q_end = to.q - 1;
-	if (to.q == first) {  // the stop is the row's first pair: that row is not sieved
-		p_hi = to.p - 1;
-		q_end = 0;
-	}
-	if (p_hi < from.p) return d;
-	d.block_lo = from.p / 100;
-	const uint64_t nb = p_hi / 100 - from.p / 100 + 1;
+	const uint64_t nb = p_hi / 100 - p_lo / 100 + 1;
 	d.block_rmax.assign(nb, 0);
 	uint64_t cap = 1 << 16;
 	for (;;) {
 		d.surv.assign(2 * cap, 0);
-		const int rc = cgpu_sieve_span(c.get(), from.p, from.q, p_hi, q_end, d.counts, d.hist.data(),
-		                               d.block_rmax.data(), nb, d.surv.data(), cap);
+		const int rc = call(d.counts, d.hist.data(), d.block_rmax.data(), nb, d.surv.data(), cap);
 		if (rc == CGPU_ERR_CAPACITY && d.counts[1] > cap) {
 			cap = d.counts[1];
 			continue;
@@ -254,6 +312,82 @@ inline DeviceScan run_span(Context& c, const SieveSet& set, SearchPair from, Sea
 	d.surv.resize(2 * d.counts[1]);
 	return d;
 }
+
+template <class Ctx>
+void check_resident(Ctx& c, const SieveSet& set)
+{
+	if (c.loaded_primes() != set.prime_count())  // the histogram is sized by the set
+		throw std::logic_error("cuboid::gpu: resident tables are not the scanned set");
+}
+
+// Whole rows p_lo..p_hi (REGION from q_start on the first row, or TRIANGLE).
+template <class Ctx>
+DeviceScan run(Ctx& c, const SieveSet& set, uint64_t p_lo, uint64_t q_start, uint64_t p_hi, int mode)
+{
+	check_resident(c, set);
+	return collect(set, p_lo, p_hi, [&](uint64_t* cnt, uint64_t* h, uint32_t* b, uint64_t nb, uint64_t* sv,
+	                                    uint64_t cap) {
+		return c.sieve(p_lo, q_start, p_hi, mode, cnt, h, b, nb, sv, cap);
+	});
+}
+
+// REGION pairs from `from` up to, not including, `to`.
+template <class Ctx>
+DeviceScan run_span(Ctx& c, const SieveSet& set, SearchPair from, SearchPair to)
+{
+	check_resident(c, set);
+	const uint64_t first = to.p == from.p ? from.q : q_bounds(to.p).q_low;
+	uint64_t p_hi = to.p, q_end = to.q - 1;
+	if (to.q == first) {  // `to` is its row's first pair: that row is not sieved
+		p_hi = to.p - 1;
+		q_end = 0;
+	}
+	if (p_hi < from.p) {
+		DeviceScan d;
+		d.hist.assign(set.prime_count(), 0);
+		return d;
+	}
+	return collect(set, from.p, p_hi, [&](uint64_t* cnt, uint64_t* h, uint32_t* b, uint64_t nb, uint64_t* sv,
+	                                      uint64_t cap) {
+		return c.sieve_span(from.p, from.q, p_hi, q_end, cnt, h, b, nb, sv, cap);
+	});
+}
+
+// Walks the reference's q visiting order (engine.hpp:225-247: rows p, q from
+// q_low(p) -- or start.q on the first row -- to q_high(p)) k steps from
+// `pos`: the pair reached, or false if p_end's row ends first. One O(1) step
+// per row (q_low moves monotonically), so a tile of 2^37 q costs microseconds.
+class Visit {
+public:
+	explicit Visit(uint64_t p_end) : p_end_(p_end) {}
+	bool advance(SearchPair pos, uint64_t k, SearchPair& at)
+	{
+		uint64_t p = pos.p, q0 = pos.q;
+		for (;;) {
+			const uint64_t q_hi = q_bounds(p).q_high;
+			const uint64_t n = q_hi >= q0 ? q_hi - q0 + 1 : 0;
+			if (k < n) {
+				at = {p, q0 + k};
+				return true;
+			}
+			k -= n;
+			if (p >= p_end_) return false;
+			++p;
+			q0 = q_low_of(p);
+		}
+	}
+
+private:
+	uint64_t q_low_of(uint64_t p)
+	{
+		if (p < kRegionCrossover) return q_bounds(p).q_low;
+		if (c_ == 0) c_ = q_bounds(p).q_low;
+		while (9 * static_cast<unsigned __int128>(c_) * c_ * c_ < p) ++c_;  // least q with 9q^3 >= p
+		return c_;
+	}
+	uint64_t p_end_;
+	uint64_t c_ = 0;
+};
 
 inline void fold(const SieveSet& set, const DeviceScan& d, ScanStats& st, const ScanSink& sink)
 {
@@ -273,10 +407,57 @@ inline void fold(const SieveSet& set, const DeviceScan& d, ScanStats& st, const 
 		}
 }
 
-}  // namespace detail
+// Mirrors the caller's std::atomic<bool> stop flag into a mapped host word the
+// kernels poll, for the lifetime of one scan.
+class StopMirror {
+public:
+	template <class Ctx>
+	StopMirror(Ctx& c, const std::atomic<bool>* flag) : flag_(flag)
+	{
+		if (!flag_) return;
+		check(cgpu_alloc_stop_word(&word_), "cgpu_alloc_stop_word");
+		attach_ = [&c](uint32_t* w) { c.set_stop_word(w); };
+		attach_(word_);
+		if (flag_->load(std::memory_order_relaxed)) *reinterpret_cast<volatile uint32_t*>(word_) = 1;  // pre-armed
+		watcher_ = std::thread([this] {
+			while (!done_.load(std::memory_order_relaxed)) {
+				if (flag_->load(std::memory_order_relaxed)) {
+					*reinterpret_cast<volatile uint32_t*>(word_) = 1;
+					return;
+				}
+				std::this_thread::sleep_for(std::chrono::microseconds(20));
+			}
+		});
+	}
+	~StopMirror()
+	{
+		disarm();
+		if (word_) cgpu_free_stop_word(word_);
+	}
+	bool raised() const { return word_ && *reinterpret_cast<volatile uint32_t*>(word_) != 0; }
+	// Stops mirroring and detaches the word, so the exact re-sieve up to the
+	// stop point runs to completion.
+	void disarm()
+	{
+		if (!flag_ || disarmed_) return;
+		disarmed_ = true;
+		done_.store(true);
+		if (watcher_.joinable()) watcher_.join();
+		attach_(nullptr);
+	}
 
-inline ScanStats scan(const SieveSet& set, SearchPair start, uint64_t p_end, const ScanSink& sink = {},
-                      const ScanOptions& opt = {}, int device = 0)
+private:
+	const std::atomic<bool>* flag_;
+	uint32_t* word_ = nullptr;
+	std::function<void(uint32_t*)> attach_;
+	std::atomic<bool> done_{false};
+	bool disarmed_ = false;
+	std::thread watcher_;
+};
+
+template <class Ctx>
+ScanStats scan_on(Ctx& c, const SieveSet& set, SearchPair start, uint64_t p_end, const ScanSink& sink,
+                  const ScanOptions& opt)
 {
 	if (set.empty()) throw ScanRejected(6);
 	if (int code = validate_start(true, start.p, start.q, opt)) throw ScanRejected(code);
@@ -287,47 +468,111 @@ inline ScanStats scan(const SieveSet& set, SearchPair start, uint64_t p_end, con
 	st.resume_p = start.p;
 	st.resume_q = start.q;
 	const auto t0 = std::chrono::steady_clock::now();
-	Context& c = context(device);
 	std::lock_guard<std::mutex> lk(c.mutex());
 	c.ensure_resident(set);
+	auto publish = [&](uint64_t p, uint64_t q) {  // flush_hooks (engine.hpp:218-223)
+		if (opt.hooks.current_p) opt.hooks.current_p->store(p, std::memory_order_relaxed);
+		if (opt.hooks.current_q) opt.hooks.current_q->store(q, std::memory_order_relaxed);
+		if (opt.hooks.current_r_max) {
+			const auto it = st.block_r_max.find(p / 100);
+			opt.hooks.current_r_max->store(it == st.block_r_max.end() ? 1 : it->second,
+			                               std::memory_order_relaxed);
+		}
+	};
+	auto finish = [&](uint64_t p_last) {  // the whole range is done: resume after p_end
+		cuboid::detail::next_pair(p_last, q_bounds(p_last).q_high, q_bounds(p_last).q_high, st.resume_p,
+		                          st.resume_q);
+		publish(p_last, q_bounds(p_last).q_high);
+	};
 
-	SearchPair at{};
-	if (opt.hooks.stop && opt.hooks.stop->load(std::memory_order_relaxed) &&
-	    detail::stop_point(start, p_end, opt.batch_pairs, at)) {
-		detail::fold(set, detail::run_span(c, set, start, at), st, sink);
+	if (start.p > p_end) {  // the reference's row loop does not run
+		st.elapsed = std::chrono::steady_clock::now() - t0;
+		return st;
+	}
+	if (!opt.hooks.stop) {  // no flag to poll: one launch
+		fold(set, run(c, set, start.p, start.q, p_end, CGPU_REGION), st, sink);
+		finish(p_end);
+		st.elapsed = std::chrono::steady_clock::now() - t0;
+		return st;
+	}
+
+	// Stoppable: tiles ending at poll points (every batch_pairs-th q visited).
+	const uint64_t B = opt.batch_pairs ? opt.batch_pairs : 1;
+	const uint64_t K = std::max<uint64_t>(1, kStopTilePairs / B);  // batches per tile
+	StopMirror mirror(c, opt.hooks.stop);
+	Visit visit(p_end);
+	SearchPair pos = start;
+	bool at_poll = false;  // pos is a poll point (not the scan start)
+	auto stop_at = [&](SearchPair at) {
+		fold(set, run_span(c, set, pos, at), st, sink);
 		st.block_r_max.try_emplace(at.p / 100, 1u);  // the stop row's block was entered
 		st.resume_p = at.p;
 		st.resume_q = at.q;
 		st.stopped = true;
-		st.elapsed = std::chrono::steady_clock::now() - t0;
-		return st;
-	}
-	uint64_t p = start.p, q = start.q;
-	while (p <= p_end) {
-		if (opt.hooks.stop && opt.hooks.stop->load(std::memory_order_relaxed)) {
+		publish(at.p, at.q);
+	};
+	for (;;) {
+		if (at_poll && opt.hooks.stop->load(std::memory_order_relaxed)) {  // the reference's poll at pos
+			st.block_r_max.try_emplace(pos.p / 100, 1u);
+			st.resume_p = pos.p;
+			st.resume_q = pos.q;
 			st.stopped = true;
+			publish(pos.p, pos.q);
 			break;
 		}
-		const uint64_t hi = opt.hooks.stop ? detail::tile_end(p, p_end) : p_end;
-		const detail::DeviceScan d = detail::run(c, set, p, q, hi, CGPU_REGION);
-		detail::fold(set, d, st, sink);
-		cuboid::detail::next_pair(hi, q_bounds(hi).q_high, q_bounds(hi).q_high, st.resume_p, st.resume_q);
-		if (opt.hooks.current_p) opt.hooks.current_p->store(hi, std::memory_order_relaxed);
-		if (opt.hooks.current_q) opt.hooks.current_q->store(q_bounds(hi).q_high, std::memory_order_relaxed);
-		if (opt.hooks.current_r_max) {
-			const auto it = st.block_r_max.find(hi / 100);
-			opt.hooks.current_r_max->store(it == st.block_r_max.end() ? 1 : it->second,
-			                               std::memory_order_relaxed);
+		// the tile: from pos up to the K-th poll point after it (the first poll
+		// point after the start is the B-th q visited, position B - 1)
+		SearchPair to{};
+		const uint64_t steps = at_poll ? K * B : K * B - 1;
+		const bool inside = visit.advance(pos, steps, to);
+		const DeviceScan d = inside ? run_span(c, set, pos, to) : run(c, set, pos.p, pos.q, p_end, CGPU_REGION);
+		if (mirror.raised()) {  // the tile may have been abandoned: halt at the next poll point instead
+			mirror.disarm();
+			SearchPair nxt{};
+			if (visit.advance(pos, at_poll ? B : B - 1, nxt)) {
+				stop_at(nxt);
+			} else {  // no poll left before p_end: the reference completes the range
+				fold(set, run(c, set, pos.p, pos.q, p_end, CGPU_REGION), st, sink);
+				finish(p_end);
+			}
+			break;
 		}
-		p = st.resume_p;
-		q = st.resume_q;
+		fold(set, d, st, sink);
+		if (!inside) {
+			finish(p_end);
+			break;
+		}
+		pos = to;
+		at_poll = true;
+		st.resume_p = pos.p;
+		st.resume_q = pos.q;
+		publish(pos.p, pos.q);
 	}
 	st.elapsed = std::chrono::steady_clock::now() - t0;
 	return st;
 }
 
+}  // namespace detail
+
+// scan() (engine.hpp:195-295) on one GPU.
+inline ScanStats scan(const SieveSet& set, SearchPair start, uint64_t p_end, const ScanSink& sink = {},
+                      const ScanOptions& opt = {}, int device = 0)
+{
+	if (set.empty()) throw ScanRejected(6);
+	return detail::scan_on(context(device), set, start, p_end, sink, opt);
+}
+
+// scan() over several GPUs of this process (block-cyclic p/100 shards, NCCL).
+inline ScanStats scan(const SieveSet& set, SearchPair start, uint64_t p_end, const ScanSink& sink,
+                      const ScanOptions& opt, const std::vector<int>& devices)
+{
+	if (set.empty()) throw ScanRejected(6);
+	if (devices.size() <= 1) return scan(set, start, p_end, sink, opt, devices.empty() ? 0 : devices[0]);
+	return detail::scan_on(multi_context(devices), set, start, p_end, sink, opt);
+}
+
 inline ScanStats scan_triangle(const SieveSet& set, uint64_t p_lo, uint64_t p_hi, const ScanSink& sink = {},
-                               int device = 0)
+                               const std::vector<int>& devices = {0})
 {
 	if (set.empty()) throw ScanRejected(6);
 	if (p_lo == 0 || p_hi > UINT32_MAX) throw ScanRejected(3);
@@ -336,14 +581,173 @@ inline ScanStats scan_triangle(const SieveSet& set, uint64_t p_lo, uint64_t p_hi
 	st.resume_q = 1;
 	const auto t0 = std::chrono::steady_clock::now();
 	if (p_lo <= p_hi) {
-		Context& c = context(device);
-		std::lock_guard<std::mutex> lk(c.mutex());
-		c.ensure_resident(set);
-		detail::fold(set, detail::run(c, set, p_lo, 0, p_hi, CGPU_TRIANGLE), st, sink);
+		auto go = [&](auto& c) {
+			std::lock_guard<std::mutex> lk(c.mutex());
+			c.ensure_resident(set);
+			detail::fold(set, detail::run(c, set, p_lo, 0, p_hi, CGPU_TRIANGLE), st, sink);
+		};
+		if (devices.size() > 1)
+			go(multi_context(devices));
+		else
+			go(context(devices.empty() ? 0 : devices[0]));
 		st.resume_p = p_hi + 1;
 	}
 	st.elapsed = std::chrono::steady_clock::now() - t0;
 	return st;
 }
+
+// ---- the search controller (engine.hpp:429-595) on the GPU ----------------------
+//
+// Same interface, status codes and files as cuboid::SearchController: load /
+// release / start / stop / status / last_stats / last_error, the report line
+// (report_append) and the FNV-digested checkpoint (checkpoint_write) written
+// with the reference's own functions when a scan ends or is stopped. The
+// worker runs gpu::scan over Config::devices. A checkpoint's (p, q) resumes
+// with start(p, q); merge of the halves equals the uninterrupted scan.
+class SearchController {
+public:
+	struct Config {
+		std::string report_path = "Cuboid_search_report.txt";
+		std::string checkpoint_path = "Cuboid_search_checkpoint.txt";
+		uint64_t p_limit = p_limit_32bit();
+		uint64_t p_end = 0;  // 0: run to p_limit
+		bool small_p = false;
+		uint64_t batch_pairs = 1u << 16;
+		ScanSink sink;                 // survivor events, delivered on the worker thread
+		std::vector<int> devices{0};   // GPUs this process drives
+	};
+
+	SearchController() = default;
+	explicit SearchController(Config cfg) : cfg_(std::move(cfg)) {}
+	~SearchController()
+	{
+		stop_.store(true);
+		join();
+	}
+	SearchController(const SearchController&) = delete;
+	SearchController& operator=(const SearchController&) = delete;
+
+	// Index file size on first load, 0 if already loaded (engine.hpp:465-474).
+	long load(const std::string& tables_path, const std::string& index_path)
+	{
+		std::lock_guard<std::mutex> lk(mu_);
+		if (set_) return 0;
+		const auto index_bytes = read_bytes(index_path);
+		const auto table_bytes = read_bytes(tables_path);
+		set_ = load_sieve(table_bytes, index_bytes);
+		return static_cast<long>(index_bytes.size());
+	}
+	// Adopts an already built set (e.g. gpu::build_set), as load() would.
+	void adopt(SieveSet set)
+	{
+		std::lock_guard<std::mutex> lk(mu_);
+		if (!set_) set_ = std::move(set);
+	}
+	int release()  // 0 released, 1 running, 6 not loaded
+	{
+		std::lock_guard<std::mutex> lk(mu_);
+		if (running_.load()) return 1;
+		join();
+		if (!set_) return 6;
+		set_.reset();
+		return 0;
+	}
+	int start(uint64_t p, uint64_t q)  // 0 started, 1 running, 2..6 validate_start
+	{
+		std::lock_guard<std::mutex> lk(mu_);
+		if (running_.load()) return 1;
+		join();
+		const ScanOptions opt = options();
+		if (int code = validate_start(set_.has_value(), p, q, opt)) return code;
+		stop_.store(false);
+		cur_p_.store(p);
+		cur_q_.store(q);
+		cur_rmax_.store(1);
+		running_.store(true);
+		worker_ = std::thread([this, p, q, opt] { run({p, q}, opt); });
+		return 0;
+	}
+	int stop()  // 0 stopped (report + checkpoint written), 1 not running
+	{
+		std::lock_guard<std::mutex> lk(mu_);
+		if (!running_.load()) return 1;
+		stop_.store(true);
+		join();
+		return 0;
+	}
+	ControllerStatus status() const
+	{
+		ControllerStatus s;
+		s.running = running_.load();
+		s.current_p_exact = cur_p_.load();
+		s.current_p = s.current_p_exact - s.current_p_exact % 100;
+		s.current_r_max = cur_rmax_.load();
+		return s;
+	}
+	bool loaded() const
+	{
+		std::lock_guard<std::mutex> lk(mu_);
+		return set_.has_value();
+	}
+	ScanStats last_stats() const
+	{
+		std::lock_guard<std::mutex> lk(stats_mu_);
+		return stats_;
+	}
+	std::string last_error() const
+	{
+		std::lock_guard<std::mutex> lk(stats_mu_);
+		return error_;
+	}
+
+private:
+	ScanOptions options()
+	{
+		ScanOptions o;
+		o.small_p = cfg_.small_p;
+		o.p_limit = cfg_.p_limit;
+		o.batch_pairs = cfg_.batch_pairs;
+		o.hooks = {&stop_, &cur_p_, &cur_q_, &cur_rmax_};
+		return o;
+	}
+	void run(SearchPair start, const ScanOptions& opt)
+	{
+		const uint64_t p_end = cfg_.p_end ? cfg_.p_end : cfg_.p_limit;
+		try {
+			ScanStats st = gpu::scan(*set_, start, p_end, cfg_.sink, opt, cfg_.devices);
+			SearchCheckpoint cp;
+			cp.p = st.resume_p;
+			cp.q = st.resume_q;
+			cp.r_max = cur_rmax_.load();
+			cp.timestamp = iso8601_local_now();
+			cp.pairs_tested = st.pairs_tested;
+			cp.survivors = st.survivors;
+			report_append(cfg_.report_path, cp);
+			checkpoint_write(cp, cfg_.checkpoint_path);
+			std::lock_guard<std::mutex> lk(stats_mu_);
+			stats_ = std::move(st);
+			error_.clear();
+		} catch (const std::exception& e) {
+			std::lock_guard<std::mutex> lk(stats_mu_);
+			error_ = e.what();
+		}
+		running_.store(false);
+	}
+	void join()
+	{
+		if (worker_.joinable()) worker_.join();
+	}
+
+	Config cfg_;
+	mutable std::mutex mu_;
+	std::optional<SieveSet> set_;
+	std::thread worker_;
+	std::atomic<bool> running_{false}, stop_{false};
+	std::atomic<uint64_t> cur_p_{0}, cur_q_{0};
+	std::atomic<uint32_t> cur_rmax_{1};
+	mutable std::mutex stats_mu_;
+	ScanStats stats_;
+	std::string error_;
+};
 
 }  // namespace cuboid::gpu

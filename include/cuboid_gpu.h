@@ -73,6 +73,8 @@ const char* cgpu_version(void);
 /* One context per device (one process per GPU). `stream` may be NULL (the
  * context creates its own) or a cudaStream_t owned by the caller. */
 int cgpu_create(int device, void* stream, cgpu_ctx** out);
+/* CUDA devices visible to this process (0 on a box without a GPU). */
+int cgpu_device_count(int* n);
 int cgpu_destroy(cgpu_ctx* ctx);
 int cgpu_set_stream(cgpu_ctx* ctx, void* stream);
 int cgpu_synchronize(cgpu_ctx* ctx);
@@ -188,6 +190,26 @@ int cgpu_sieve_span(cgpu_ctx* ctx, uint64_t p_lo, uint64_t q_start, uint64_t p_h
                     uint64_t* counts, uint64_t* hist, uint32_t* block_rmax, uint64_t block_cap,
                     uint64_t* surv_pq, uint64_t surv_cap);
 
+/* cgpu_sieve_launch_dev for a REGION span that may end mid-row (as
+ * cgpu_sieve_span: rows p_lo..p_hi, the first from q_start, the last up to
+ * q_end inclusive, 0 = q_high), restricted to the block-cyclic shard. */
+int cgpu_sieve_launch_span_dev(cgpu_ctx* ctx, uint64_t p_lo, uint64_t q_start, uint64_t p_hi,
+                               uint64_t q_end, uint32_t shard_count, uint32_t shard_index,
+                               uint64_t* d_counts, uint64_t* d_hist, uint32_t* d_block_rmax,
+                               uint64_t block_cap, uint64_t* d_surv, uint64_t surv_cap);
+
+/* Cooperative stop (ScanOptions::hooks.stop, engine.hpp:137-149, 248-257) that
+ * the DEVICE sees. cgpu_alloc_stop_word returns a zeroed host word in mapped,
+ * portable pinned memory; after cgpu_set_stop_word(ctx, word) every sieve
+ * launch of ctx polls it (each warp, every 8th row) and abandons its
+ * remaining rows once it is nonzero. The results of a launch that saw the
+ * word raised are INCOMPLETE: the caller discards them and sieves exactly up
+ * to the reference's next stop point with a span (include/cuboid/gpu.hpp
+ * does). word = NULL detaches. */
+int cgpu_alloc_stop_word(uint32_t** word);
+int cgpu_free_stop_word(uint32_t* word);
+int cgpu_set_stop_word(cgpu_ctx* ctx, uint32_t* word);
+
 /* Device time of the last sieve launch or table build, from CUDA events on the
  * context stream (waits for them). Sieve: ms[0] = init + first plan kernel,
  * ms[1] = sieve kernel(s), ms[2] = whole launch. Table build: ms[0] = build
@@ -216,6 +238,44 @@ int cgpu_last_launch_count(cgpu_ctx* ctx, uint32_t* n);
  * engine.hpp:72-78): out_rank[i] = rank of the smallest-rank prime whose table
  * rejects (p_i, q_i), or -1 if no table does. pq = n pairs of u64 (p, q). */
 int cgpu_classify(cgpu_ctx* ctx, const uint64_t* pq, uint64_t n, int32_t* out_rank);
+
+/* ---- in-process multi-GPU (one process, G devices, NCCL) ------------------ */
+
+/* The reference drives its search from ONE process (scan() on the
+ * SearchController's worker thread, engine.hpp:494, 555-577); this is how that
+ * process uses every GPU of the box. One cgpu_ctx and stream per device, one
+ * NCCL clique from ncclCommInitAll over `devices` (NULL = 0..n-1; each device
+ * at most once). Rows are sharded block-cyclically by p/100 block
+ * (SURVEY.md 8(e)), so each reference r_max block lives on one device. */
+typedef struct cgpu_multi cgpu_multi;
+
+int cgpu_multi_create(int n_devices, const int* devices, cgpu_multi** out);
+int cgpu_multi_destroy(cgpu_multi* m);
+int cgpu_multi_size(cgpu_multi* m, int* n);
+/* The i-th device's context (borrowed; it holds the full set after a load). */
+int cgpu_multi_ctx(cgpu_multi* m, int i, cgpu_ctx** out);
+
+/* As cgpu_tables_load on every device: each copies 1/G of the host bytes over
+ * its own PCIe link and an in-place ncclAllGather assembles the set. */
+int cgpu_multi_tables_load(cgpu_multi* m, const uint32_t* primes, uint32_t n, const uint8_t* bytes,
+                           uint64_t nbytes);
+
+/* Synchronous multi-GPU cgpu_sieve (shard arguments implied): device g sieves
+ * the blocks with (p/100) % G == g; one grouped NCCL all-reduce merges the
+ * counters and histogram (SUM, ScanStats::merge engine.hpp:121-134) and block
+ * r_max (MAX); grouped ncclSend/ncclRecv gather the survivor lists onto the
+ * first device; outputs as cgpu_sieve_results (survivors ascending). q_end != 0
+ * ends a REGION span mid-row (as cgpu_sieve_span). */
+int cgpu_multi_sieve(cgpu_multi* m, uint64_t p_lo, uint64_t q_start, uint64_t p_hi, uint64_t q_end,
+                     int mode, uint64_t* counts, uint64_t* hist, uint32_t* block_rmax, uint64_t block_cap,
+                     uint64_t* surv_pq, uint64_t surv_cap);
+
+/* cgpu_set_stop_word on every device's context (one portable word). */
+int cgpu_multi_set_stop_word(cgpu_multi* m, uint32_t* word);
+
+/* Device time of the last cgpu_multi_sieve, max over devices (CUDA events on
+ * each device's stream, from its launch to its last result copy). */
+int cgpu_multi_last_ms(cgpu_multi* m, float* ms);
 
 /* ---- region arithmetic (host) -------------------------------------------- */
 

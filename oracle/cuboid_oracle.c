@@ -212,8 +212,11 @@ static uint64_t gcd_u64(uint64_t a, uint64_t b)
  * [1, p-1], the loop of verify_small_region, engine.hpp:613-625).
  * The first row starts at q_start when q_start != 0 (engine.hpp:227).
  * Per pair: skip q == p or gcd(p,q) > 1 (engine.hpp:258); count it
- * (engine.hpp:259); probe primes in rank order, skipping those with
- * p mod r == 0 (engine.hpp:242), first set bit kills (engine.hpp:261-269).
+ * (engine.hpp:259); probe primes in rank order, first set bit kills
+ * (engine.hpp:261-269). REGION skips primes with p mod r == 0
+ * (engine.hpp:240-242); TRIANGLE (the verify_small_region loop over
+ * is_unsolvable, engine.hpp:619-623, sievetable.hpp:199-205) probes row 0 like
+ * any other row -- the two differ only for tables with bits in row 0.
  * Outputs: hist[rank] of first killers, row_rmax[p - p_lo] = largest killer
  * prime in the row or 1 (engine.hpp:229-236, 271), and survivors as (p,q)
  * pairs in ascending order. Returns 0.
@@ -240,7 +243,7 @@ int co_sieve(const uint8_t* tables, const uint32_t* primes, const uint32_t* offs
 		if (p == p_lo && q_start) lo = q_start;
 		for (uint32_t k = 0; k < n; ++k) {
 			const uint32_t a = (uint32_t)(p % primes[k]);
-			if (a == 0) continue;
+			if (a == 0 && mode == 0) continue;
 			prm[np] = primes[k];
 			rk[np] = k;
 			rowoff[np] = a * primes[k];

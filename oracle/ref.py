@@ -63,6 +63,9 @@ def lib():
                                     _u64p, _u64p, _u64p, _u32p, C.c_uint64, _u64p, _u64p, _i32p,
                                     C.c_uint64, _u64p, C.POINTER(C.c_double)]
         L.cref_verify_small_region.argtypes = [C.c_void_p, _u64p]
+        L.cref_classify.argtypes = [C.c_void_p, C.c_void_p, C.c_uint64, C.c_int, C.c_void_p]
+        L.cref_build_tables.argtypes = [C.c_void_p, C.c_uint32, C.c_int, C.c_int, C.c_void_p,
+                                        C.c_void_p, C.POINTER(C.c_double)]
         _lib = L
     return _lib
 
@@ -258,3 +261,28 @@ def verify_small_region(rset):
     _check(lib().cref_verify_small_region(rset.h, out))
     keys = ("pairs", "sieved_out", "survivors", "no_integer_root", "root_fails", "candidates")
     return {k: out[i] for i, k in enumerate(keys)}
+
+
+def classify(rset, pq, nthreads=1):
+    """First-killer rank per (p, q) row of the (n, 2) uint64 array pq (-1 =
+    survivor) through SieveSet::is_unsolvable in rank order."""
+    import numpy as np
+    pq = np.ascontiguousarray(pq, dtype=np.uint64)
+    out = np.empty(len(pq), np.int32)
+    _check(lib().cref_classify(rset.h, pq.ctypes.data, len(pq), nthreads, out.ctypes.data))
+    return out
+
+
+def build_tables(primes, oracle=False, nthreads=1):
+    """The reference builders (build_table / build_table_oracle) over `primes`
+    into one SieveSet-layout byte string; returns (bytes, elapsed seconds)."""
+    import numpy as np
+    P = np.ascontiguousarray(primes, dtype=np.uint32)
+    sizes = (P.astype(np.uint64) ** 2 + 7) // 8
+    offs = np.zeros(len(P), np.uint64)
+    offs[1:] = np.cumsum(sizes)[:-1]
+    out = np.zeros(int(sizes.sum()), np.uint8)
+    el = C.c_double()
+    _check(lib().cref_build_tables(P.ctypes.data, len(P), int(oracle), nthreads, offs.ctypes.data,
+                                   out.ctypes.data, C.byref(el)))
+    return out.tobytes(), el.value

@@ -13,6 +13,7 @@
 // engine.hpp:121-134).
 
 #include <algorithm>
+#include <chrono>
 #include <atomic>
 #include <cstdint>
 #include <cstring>
@@ -165,6 +166,69 @@ int cref_build_table_oracle(uint32_t r, uint8_t* out)
 	try {
 		const BitTable t = build_table_oracle(r);
 		std::memcpy(out, t.bytes.data(), t.bytes.size());
+		return 0;
+	} catch (const std::exception& e) {
+		return fail(e);
+	}
+}
+
+// Rank-ordered first killer of explicit pairs through SieveSet::is_unsolvable
+// (sievetable.hpp:199-205) -- the sieve part of verify_pair (engine.hpp:72-78);
+// -1 when no table rejects the pair. Pairs split over `nthreads` threads.
+int cref_classify(void* sp, const uint64_t* pq, uint64_t n, int nthreads, int32_t* out)
+{
+	try {
+		const SieveSet& set = *static_cast<SieveSet*>(sp);
+		const size_t nprimes = set.prime_count();
+		if (nthreads < 1) nthreads = 1;
+		std::vector<std::thread> th;
+		for (int t = 0; t < nthreads; ++t)
+			th.emplace_back([&, t] {
+				for (uint64_t i = t; i < n; i += nthreads) {
+					int32_t rank = -1;
+					for (size_t k = 0; k < nprimes; ++k)
+						if (set.is_unsolvable(k, pq[2 * i], pq[2 * i + 1])) {
+							rank = static_cast<int32_t>(k);
+							break;
+						}
+					out[i] = rank;
+				}
+			});
+		for (auto& x : th) x.join();
+		return 0;
+	} catch (const std::exception& e) {
+		return fail(e);
+	}
+}
+
+// The reference's builders over a prime list (production build_table,
+// sievetable.hpp:123-141, or the definition build_table_oracle, :102-115),
+// primes claimed dynamically by `nthreads` threads; tables written at the
+// set's offsets (SieveSet::build layout, :159-176). Returns 0.
+int cref_build_tables(const uint32_t* primes, uint32_t n, int oracle, int nthreads,
+                      const uint64_t* offsets, uint8_t* out, double* elapsed_s)
+{
+	try {
+		if (nthreads < 1) nthreads = 1;
+		std::atomic<uint32_t> next{0};
+		std::vector<std::string> errs(nthreads);
+		const auto t0 = std::chrono::steady_clock::now();
+		std::vector<std::thread> th;
+		for (int t = 0; t < nthreads; ++t)
+			th.emplace_back([&, t] {
+				try {
+					for (uint32_t k; (k = next.fetch_add(1)) < n;) {
+						const BitTable b = oracle ? build_table_oracle(primes[k]) : build_table(primes[k]);
+						std::memcpy(out + offsets[k], b.bytes.data(), b.bytes.size());
+					}
+				} catch (const std::exception& e) {
+					errs[t] = e.what();
+				}
+			});
+		for (auto& x : th) x.join();
+		for (auto& e : errs)
+			if (!e.empty()) throw std::runtime_error(e);
+		*elapsed_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
 		return 0;
 	} catch (const std::exception& e) {
 		return fail(e);

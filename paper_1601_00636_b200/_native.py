@@ -28,6 +28,7 @@ SIGNATURES = {
     "cgpu_version": (C.c_char_p, []),
     "cgpu_create": (C.c_int, [C.c_int, C.c_void_p, C.POINTER(C.c_void_p)]),
     "cgpu_destroy": (C.c_int, [C.c_void_p]),
+    "cgpu_device_count": (C.c_int, [C.POINTER(C.c_int)]),
     "cgpu_set_stream": (C.c_int, [C.c_void_p, C.c_void_p]),
     "cgpu_synchronize": (C.c_int, [C.c_void_p]),
     "cgpu_table_layout": (C.c_int, [C.c_void_p, C.c_uint32, C.c_void_p, _u64p]),
@@ -57,6 +58,21 @@ SIGNATURES = {
                                   C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p,
                                   C.c_uint64]),
     "cgpu_last_timings": (C.c_int, [C.c_void_p, C.POINTER(C.c_float)]),
+    "cgpu_multi_create": (C.c_int, [C.c_int, C.c_void_p, C.POINTER(C.c_void_p)]),
+    "cgpu_multi_destroy": (C.c_int, [C.c_void_p]),
+    "cgpu_multi_size": (C.c_int, [C.c_void_p, C.POINTER(C.c_int)]),
+    "cgpu_multi_ctx": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_void_p)]),
+    "cgpu_multi_tables_load": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint32, C.c_void_p, C.c_uint64]),
+    "cgpu_multi_sieve": (C.c_int, [C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64, C.c_int,
+                                   C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint64]),
+    "cgpu_multi_set_stop_word": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "cgpu_sieve_launch_span_dev": (C.c_int, [C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64,
+                                             C.c_uint32, C.c_uint32, C.c_void_p, C.c_void_p, C.c_void_p,
+                                             C.c_uint64, C.c_void_p, C.c_uint64]),
+    "cgpu_alloc_stop_word": (C.c_int, [C.POINTER(C.c_void_p)]),
+    "cgpu_free_stop_word": (C.c_int, [C.c_void_p]),
+    "cgpu_set_stop_word": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "cgpu_multi_last_ms": (C.c_int, [C.c_void_p, C.POINTER(C.c_float)]),
     "cgpu_int32_peak": (C.c_int, [C.c_int, C.POINTER(C.c_double)]),
     "cgpu_fp32_peak": (C.c_int, [C.c_int, C.POINTER(C.c_double)]),
     "cgpu_last_launch_count": (C.c_int, [C.c_void_p, _u32p]),

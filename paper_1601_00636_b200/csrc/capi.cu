@@ -122,6 +122,9 @@ constexpr uint32_t kBlocksPerLaunch = kMaxSlots / 100;
 
 }  // namespace
 
+// shared with multi.cu (internal.cuh)
+int cgpu_internal_set_err(int code, const std::string& msg) { return set_err(code, msg); }
+
 struct cgpu_ctx {
 	int device = 0;
 	cudaStream_t stream = nullptr;
@@ -132,6 +135,10 @@ struct cgpu_ctx {
 	bool loaded = false;
 	std::vector<uint32_t> primes, offsets, ext_base;
 	std::vector<uint8_t> killable;
+	// row 0 (p = 0 mod r) of the derived layout: zeroed for REGION (scan()
+	// skips those primes, engine.hpp:240-242), as loaded for TRIANGLE when a
+	// non-canonical set has bits there (is_unsolvable reads it)
+	bool keep_row0 = false, row0_nonzero = false;
 	uint64_t total_bytes = 0, ext_words = 0;
 	DevBuf<uint8_t> packed;
 	DevBuf<uint32_t> ext, d_primes, d_offsets, killflags;
@@ -154,6 +161,9 @@ struct cgpu_ctx {
 	float drain_alpha = kDefaultDrainAlpha;
 	DevBuf<uint2> fprimes;
 	uint32_t n_fprimes = 0;
+
+	// cooperative stop word (cgpu_set_stop_word): device view of a mapped host word
+	const volatile uint32_t* stop_dev = nullptr;
 
 	// sieve buffers
 	DevBuf<unsigned long long> hist, counters, surv, prefix, chunk_off;
@@ -301,7 +311,7 @@ std::vector<PrimeJob> make_jobs(const std::vector<uint32_t>& primes,
 // build the probe list (killable tables in rank order).
 // check_padding: a k_check_padding flag was enqueued into killflags[n]; it
 // is read back with the killable flags (one host sync per load).
-int finalize_set(cgpu_ctx* c, bool check_padding = false)
+int finalize_set(cgpu_ctx* c, bool check_padding = false, bool keep_row0 = false)
 {
 	const uint32_t n = static_cast<uint32_t>(c->primes.size());
 	std::vector<PrimeJob> jobs = make_jobs(c->primes, c->offsets, c->ext_base, c->ext_words);
@@ -324,7 +334,7 @@ int finalize_set(cgpu_ctx* c, bool check_padding = false)
 		CK(cudaMemcpyAsync(c->derive_items.p, items.data(), sizeof(uint4) * items.size(), cudaMemcpyHostToDevice,
 		                   c->stream));
 		CK(launch_derive(c->jobs_rank.p, c->derive_items.p, static_cast<uint32_t>(items.size()), c->packed.p,
-		                 c->ext.p, c->killflags.p, c->stream));
+		                 c->ext.p, c->killflags.p, keep_row0 ? 1 : 0, c->stream));
 		++c->launches;
 	}
 	std::vector<uint32_t> kf(n + 1, 0);
@@ -335,10 +345,13 @@ int finalize_set(cgpu_ctx* c, bool check_padding = false)
 	c->killable.assign(n, 0);
 	c->probe_rank.clear();
 	c->probe_r.clear();
+	c->keep_row0 = keep_row0;
+	c->row0_nonzero = false;
 	std::vector<uint4> pr;
 	for (uint32_t k = 0; k < n; ++k) {
-		c->killable[k] = kf[k] ? 1 : 0;
-		if (!kf[k]) continue;  // an all-zero table never kills: skipping it is exact
+		c->row0_nonzero |= (kf[k] & 2u) != 0;
+		c->killable[k] = (kf[k] & 1u) ? 1 : 0;
+		if (!(kf[k] & 1u)) continue;  // an all-zero table never kills: skipping it is exact
 		const uint32_t r = c->primes[k];
 		c->probe_rank.push_back(k);
 		c->probe_r.push_back(r);
@@ -712,6 +725,9 @@ int check_launch(cgpu_ctx* c, uint64_t p_lo, uint64_t q_start, uint64_t p_hi, in
 	if (!c->loaded || c->primes.empty()) return set_err(CGPU_NOT_LOADED, "tables not loaded");
 	if (mode != CGPU_REGION && mode != CGPU_TRIANGLE) return set_err(CGPU_ERR_INVALID, "unknown mode");
 	if (G == 0 || g >= G) return set_err(CGPU_ERR_INVALID, "bad shard (count, index)");
+	// validate_start (engine.hpp:152-161) with small_p on: the C ABI sieves rows
+	// below 152 (the small-p region and TRIANGLE rows), so p = 0 is code 3;
+	// the C++/Python scan() wrappers apply opt.small_p first (p < 152 -> 2)
 	if (p_lo == 0) return set_err(CGPU_P_ABOVE_LIMIT, "p must be positive");
 	if (mode == CGPU_REGION) {
 		if (p_hi > kPLimit32 || p_lo > kPLimit32)
@@ -726,6 +742,9 @@ int check_launch(cgpu_ctx* c, uint64_t p_lo, uint64_t q_start, uint64_t p_hi, in
 		if (q_start) return set_err(CGPU_ERR_INVALID, "TRIANGLE mode sieves whole rows (q_start must be 0)");
 		if (p_hi > 0xffffffffull) return set_err(CGPU_P_ABOVE_LIMIT, "p above 2^32");
 	}
+	// non-canonical sets with bits in row 0: re-derive the layout the mode reads
+	const bool keep = mode == CGPU_TRIANGLE && c->row0_nonzero;
+	if (keep != c->keep_row0) return finalize_set(c, false, keep);
 	return CGPU_OK;
 }
 
@@ -786,6 +805,7 @@ int enqueue_sieve(cgpu_ctx* c, uint64_t p_lo, uint64_t q_start, uint64_t p_hi, u
 	a.blk_lo = blk_lo;
 	a.surv = d_surv;
 	a.surv_cap = surv_cap;
+	a.stop = c->stop_dev;
 
 	// owned blocks: b in [blk_lo, blk_hi] with b % G == g
 	const uint64_t blk_hi = p_hi / 100;
@@ -887,6 +907,70 @@ int cgpu_sieve_launch_dev(cgpu_ctx* c, uint64_t p_lo, uint64_t q_start, uint64_t
 	                     reinterpret_cast<unsigned long long*>(d_counts),
 	                     reinterpret_cast<unsigned long long*>(d_hist), d_block_rmax,
 	                     reinterpret_cast<unsigned long long*>(d_surv), surv_cap);
+}
+
+int cgpu_sieve_launch_span_dev(cgpu_ctx* c, uint64_t p_lo, uint64_t q_start, uint64_t p_hi, uint64_t q_end,
+                               uint32_t G, uint32_t g, uint64_t* d_counts, uint64_t* d_hist,
+                               uint32_t* d_block_rmax, uint64_t block_cap, uint64_t* d_surv, uint64_t surv_cap)
+{
+	if (int rc = check_launch(c, p_lo, q_start, p_hi, CGPU_REGION, G, g)) return rc;
+	if (q_end) {
+		uint64_t lo, hi;
+		q_bounds(p_hi, &lo, &hi);
+		if (q_end > hi) return set_err(CGPU_Q_ABOVE_HIGH, "q_end above q_high");
+	}
+	if (!d_counts || !d_hist || (!d_block_rmax && launch_blocks(p_lo, p_hi)) || (!d_surv && surv_cap))
+		return set_err(CGPU_ERR_INVALID, "null device output buffer");
+	if (block_cap < launch_blocks(p_lo, p_hi))
+		return set_err(CGPU_ERR_CAPACITY, "block_rmax buffer too small");
+	CK(cudaSetDevice(c->device));
+	c->results_internal = false;
+	return enqueue_sieve(c, p_lo, q_start, p_hi, q_end, CGPU_REGION, G, g,
+	                     reinterpret_cast<unsigned long long*>(d_counts),
+	                     reinterpret_cast<unsigned long long*>(d_hist), d_block_rmax,
+	                     reinterpret_cast<unsigned long long*>(d_surv), surv_cap);
+}
+
+int cgpu_device_count(int* n)
+{
+	if (!n) return set_err(CGPU_ERR_INVALID, "null argument");
+	*n = 0;
+	if (cudaGetDeviceCount(n) != cudaSuccess) *n = 0;
+	return CGPU_OK;
+}
+
+int cgpu_alloc_stop_word(uint32_t** word)
+{
+	if (!word) return set_err(CGPU_ERR_INVALID, "null argument");
+	*word = nullptr;
+	int count = 0;
+	if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0)
+		return set_err(CGPU_ERR_NO_DEVICE, "no CUDA device visible: cuboid_gpu has no CPU fallback");
+	void* p = nullptr;
+	CK(cudaHostAlloc(&p, 64, cudaHostAllocMapped | cudaHostAllocPortable));
+	std::memset(p, 0, 64);
+	*word = static_cast<uint32_t*>(p);
+	return CGPU_OK;
+}
+
+int cgpu_free_stop_word(uint32_t* word)
+{
+	if (word) CK(cudaFreeHost(word));
+	return CGPU_OK;
+}
+
+int cgpu_set_stop_word(cgpu_ctx* c, uint32_t* word)
+{
+	if (!c) return set_err(CGPU_ERR_INVALID, "null ctx");
+	if (!word) {
+		c->stop_dev = nullptr;
+		return CGPU_OK;
+	}
+	CK(cudaSetDevice(c->device));
+	void* d = nullptr;
+	CK(cudaHostGetDevicePointer(&d, word, 0));
+	c->stop_dev = static_cast<const volatile uint32_t*>(d);
+	return CGPU_OK;
 }
 
 int cgpu_sieve_results(cgpu_ctx* c, uint64_t* counts, uint64_t* hist, uint32_t* block_rmax,

@@ -43,7 +43,7 @@ cudaError_t launch_wintab(const uint4* d_probes, uint32_t nprobes, uint32_t entr
                           uint32_t stride, uint32_t* d_out, cudaStream_t s);
 
 cudaError_t launch_derive(const PrimeJob* d_jobs, const uint4* d_items, uint32_t nitems, const uint8_t* d_packed,
-                          uint32_t* d_ext, uint32_t* d_killable, cudaStream_t s);
+                          uint32_t* d_ext, uint32_t* d_killable, int keep_row0, cudaStream_t s);
 // k_derive work items {job, first row, rows, 0} of <= kDeriveItemWords output words each
 std::vector<uint4> derive_items(const std::vector<uint32_t>& primes);
 
@@ -151,6 +151,11 @@ struct SieveArgs {
 	uint64_t blk_lo;
 	unsigned long long* surv;          // (p << 32) | q
 	unsigned long long surv_cap;
+	// cooperative stop (engine.hpp:248-257): a mapped host word; when nonzero
+	// the sieve's warps abandon their remaining rows (checked every 8th row
+	// slot) and the launch's results are incomplete -- the caller discards
+	// them and re-sieves exactly up to the reference's next stop point
+	const volatile uint32_t* stop;
 };
 
 cudaError_t launch_plan(const SieveArgs& a, cudaStream_t s);

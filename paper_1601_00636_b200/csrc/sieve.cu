@@ -702,6 +702,7 @@ __global__ void __launch_bounds__(kSieveThreads, kSieveMinBlocks) k_sieve(const 
 		const unsigned long long u0 = ws - rs, u1 = min(we, re) - rs;
 		ws = min(we, re);
 		const uint32_t cur = slot++;
+		if (a.stop && (cur & 7u) == 0 && *a.stop) break;  // stop raised: abandon the launch
 		const uint32_t rcost = a.row_cost;
 		if (u1 <= rcost) continue;
 		const RowBounds rb = slot_row(a, cur);

@@ -349,15 +349,20 @@ __global__ void __launch_bounds__(kPermThreads) k_permute(const PrimeJob* __rest
 // output words each): the CTA stages the item's packed bits in shared memory
 // with coalesced word loads, then each thread builds output words from it
 // (one or two funnel shifts across the row wrap) and stores them coalesced;
-// killable[k] is set when any word of table k is nonzero. Row 0 is written as
-// zeros whatever the bytes hold: scan() skips primes with p mod r = 0
-// (engine.hpp:240-242), and canonical tables have a zero row 0 anyway. (Per-word gathers
-// straight from L2 were latency-bound: 113-145 us for the 256-prime set.)
+// killable[k] bit 0 is set when any word written for table k is nonzero, bit
+// 1 when the loaded row 0 holds a set bit. Row 0 is written as zeros unless
+// keep_row0: scan() skips primes with p mod r = 0 (engine.hpp:240-242), while
+// the TRIANGLE loop's is_unsolvable reads the row like any other
+// (sievetable.hpp:199-205, engine.hpp:619-623); canonical tables have a zero
+// row 0 anyway, so the two layouts differ only for non-canonical loaded bytes.
+// (Per-word gathers straight from L2 were latency-bound: 113-145 us for the
+// 256-prime set.)
 __global__ void __launch_bounds__(kDeriveThreads) k_derive(const PrimeJob* __restrict__ jobs,
                                                            const uint4* __restrict__ items,
                                                            const uint8_t* __restrict__ packed,
                                                            uint32_t* __restrict__ ext,
-                                                           uint32_t* __restrict__ killable)
+                                                           uint32_t* __restrict__ killable,
+                                                           int keep_row0)
 {
 	extern __shared__ uint32_t s_bits[];
 	const uint4 it = items[blockIdx.x];  // {job, first row, rows, -}
@@ -377,7 +382,7 @@ __global__ void __launch_bounds__(kDeriveThreads) k_derive(const PrimeJob* __res
 		const uint32_t li = i + sh;
 		return __funnelshift_r(s_bits[li >> 5], s_bits[(li >> 5) + 1], li & 31);
 	};
-	bool any = false;
+	bool any = false, row0_set = false;
 	const uint32_t words = it.z * S;
 	const uint32_t mS = barrett_m(S);
 	for (uint32_t w = threadIdx.x; w < words; w += blockDim.x) {
@@ -399,11 +404,17 @@ __global__ void __launch_bounds__(kDeriveThreads) k_derive(const PrimeJob* __res
 				b = b + 1 == r ? 0 : b + 1;
 			}
 		}
-		if (it.y + a == 0) word = 0;  // row p = 0 mod r: scan() never probes it (engine.hpp:240-242)
+		if (it.y + a == 0) {  // row p = 0 mod r: scan() never probes it (engine.hpp:240-242)
+			row0_set |= word != 0;
+			if (!keep_row0) word = 0;
+		}
 		ext[job.ext_base + static_cast<uint64_t>(it.y) * S + w] = word;
 		any |= word != 0;
 	}
-	if (__syncthreads_or(any) && threadIdx.x == 0) atomicOr(&killable[it.x], 1u);
+	const bool any_cta = __syncthreads_or(any);
+	const bool row0_cta = __syncthreads_or(row0_set);
+	if (threadIdx.x == 0 && (any_cta || row0_cta))
+		atomicOr(&killable[it.x], (any_cta ? 1u : 0u) | (row0_cta ? 2u : 0u));
 }
 
 // Window tables for the sieve's table probes: entry (j, a, b) -- for probe j
@@ -517,12 +528,12 @@ cudaError_t launch_wintab(const uint4* d_probes, uint32_t nprobes, uint32_t entr
 }
 
 cudaError_t launch_derive(const PrimeJob* d_jobs, const uint4* d_items, uint32_t nitems, const uint8_t* d_packed,
-                          uint32_t* d_ext, uint32_t* d_killable, cudaStream_t s)
+                          uint32_t* d_ext, uint32_t* d_killable, int keep_row0, cudaStream_t s)
 {
 	if (!nitems) return cudaSuccess;
 	// staged bits: <= kDeriveItemWords output words cover <= kDeriveItemWords * 32 bits... plus slack
 	const size_t smem = sizeof(uint32_t) * (kDeriveItemWords + 4);
-	k_derive<<<nitems, kDeriveThreads, smem, s>>>(d_jobs, d_items, d_packed, d_ext, d_killable);
+	k_derive<<<nitems, kDeriveThreads, smem, s>>>(d_jobs, d_items, d_packed, d_ext, d_killable, keep_row0);
 	return cudaGetLastError();
 }
 

@@ -23,6 +23,7 @@ exactly as scan() does when a sink is set (engine.hpp:272-277).
 from __future__ import annotations
 
 import ctypes as C
+import itertools
 import time
 from dataclasses import dataclass, field
 from typing import Callable, Optional
@@ -81,13 +82,18 @@ class BitTable:
 def build_table(r: int, dev: int = 0) -> BitTable:
     """One table, built on the GPU (replaces build_table, sievetable.hpp:123-141).
     ValueError (std::invalid_argument) for a modulus that is not a prime < 9697."""
+    d = device(dev)
+    d._owner = None  # the build replaces the resident tables
     try:
-        tb, _ = device(dev).build([r], N.BUILD_PRODUCTION)
+        tb, _ = d.build([r], N.BUILD_PRODUCTION)
     except N.CudaSieveError as e:
         if e.code == N.ERR_INVALID:
             raise ValueError("bit table modulus must be a prime below 9697") from e
         raise
     return BitTable(r, tb)
+
+
+_SET_SERIALS = itertools.count(1)
 
 
 class SieveSet:
@@ -98,6 +104,9 @@ class SieveSet:
         self._tables = tables
         self._offsets = [int(x) for x in offsets]
         self._dev = dev
+        # residency token: unique per set for the process lifetime (an id()
+        # can be reused by a later set once this one is collected)
+        self._serial = next(_SET_SERIALS)
 
     # -- construction ------------------------------------------------------
     @classmethod
@@ -116,7 +125,7 @@ class SieveSet:
                 raise OverflowError(str(e)) from e
             raise
         s = cls(primes, tb, d.offsets, dev)
-        d._owner = id(s)
+        d._owner = s._serial
         return s
 
     @classmethod
@@ -137,7 +146,7 @@ class SieveSet:
                 raise FormatError(str(e)) from e
             raise
         s = cls(primes, bytes(tables), d.offsets, dev)
-        d._owner = id(s)
+        d._owner = s._serial
         return s
 
     # -- queries (sievetable.hpp:181-205) ----------------------------------
@@ -196,7 +205,7 @@ class SieveSet:
                 raise OSError(str(e)) from e
             raise
         s = cls(d.primes, d.download(), d.offsets, dev)
-        d._owner = id(s)
+        d._owner = s._serial
         return s
 
     # -- device residency --------------------------------------------------
@@ -204,9 +213,10 @@ class SieveSet:
         """The device context with this set loaded (re-uploads if another set
         was made resident on the same GPU since)."""
         d = device(self._dev)
-        if getattr(d, "_owner", None) != id(self):
+        if getattr(d, "_owner", None) != self._serial:
+            d._owner = None
             d.load(self._primes, self._tables)
-            d._owner = id(self)
+            d._owner = self._serial
         return d
 
 
@@ -464,25 +474,33 @@ class SmallRegionSummary:
     candidates: int = 0
 
 
-def verify_small_region(set_: SieveSet, verifier: Optional[Callable] = None) -> SmallRegionSummary:
+def verify_small_region(set_: SieveSet, verifier: Callable) -> SmallRegionSummary:
     """verify_small_region (engine.hpp:609-640): every coprime p != q pair of
-    the region rows p <= 151, sieved on the GPU; survivors go to `verifier`
-    (p, q) -> "NoIntegerRoot" | "RootFailsInequalities" | "CuboidCandidate"
-    (the reference's exact check). A candidate raises, as in the reference."""
+    the region rows p <= 151, sieved on the GPU; every survivor goes to
+    `verifier` (p, q) -> "NoIntegerRoot" | "RootFailsInequalities" |
+    "CuboidCandidate" -- the reference's exact check, verify_pair(bypass)
+    (engine.hpp:626-635). There is no default: without the exact check the
+    survivors are unverified, so a missing verifier raises (TypeError) instead
+    of reporting them as NoIntegerRoot. A candidate raises, as in the
+    reference."""
+    if verifier is None or not callable(verifier):
+        raise TypeError("verify_small_region needs the exact final check (verifier)")
     if set_.empty():
         raise ValueError("verify_small_region: empty sieve set")
     st = scan(set_, (1, 1), 151, opt=ScanOptions(small_p=True))
     out = SmallRegionSummary(pairs=st.pairs_tested, sieved_out=st.pairs_tested - st.survivors,
                              survivors=st.survivors)
     for p, q in st.survivor_pairs:
-        kind = verifier(p, q) if verifier else "NoIntegerRoot"
+        kind = verifier(p, q)
         if kind == "CuboidCandidate":
             out.candidates += 1
             raise RuntimeError(f"cuboid candidate found at p={p}, q={q}")
         if kind == "RootFailsInequalities":
             out.root_fails += 1
-        else:
+        elif kind == "NoIntegerRoot":
             out.no_integer_root += 1
+        else:
+            raise ValueError(f"verifier returned an unknown verdict {kind!r} for ({p}, {q})")
     return out
 
 

@@ -41,12 +41,43 @@ def stats_json(st, primes, with_surv=False):
     return d
 
 
-def main():
-    g = {"generator": "oracle/_ref (reference headers, unmodified)", "tables": {}, "sieve": {}}
+def c4_subsample(g, rset, primes):
+    """C4's phi-weighted coprime 10^6-pair subsample (tests/subsample.py):
+    first-killer rank of every pair from the reference's is_unsolvable in rank
+    order (sievetable.hpp:199-205), stored as hashes plus the rank histogram."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import numpy as np
+    import subsample
+    t0 = time.time()
+    pq = subsample.sample()
+    ranks = ref.classify(rset, pq, THREADS)
+    hist = np.bincount(ranks + 1, minlength=len(primes) + 1)
+    g["sieve"]["C4_subsample"] = {
+        "set": "odd128", "seed": subsample.SEED, "n": int(len(pq)), "p_max": subsample.P_MAX,
+        "pairs_sha256": sha(pq.tobytes()), "ranks_sha256": sha(ranks.astype("<i4").tobytes()),
+        "survivors": int(hist[0]),
+        "rank_histogram": {str(primes[k]): int(c) for k, c in enumerate(hist[1:]) if c},
+    }
+    print("C4_subsample", len(pq), f"{time.time() - t0:.1f}s", flush=True)
+
+
+def main(only=()):
+    """Regenerate everything, or (with names) only those sieve entries, merged
+    into the committed golden.json (e.g. `make_golden.py C5` -- the headline
+    config, ~10 min on 8 host threads)."""
+    out = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden.json")
+    if only:
+        with open(out) as f:
+            g = json.load(f)
+    else:
+        g = {"generator": "oracle/_ref (reference headers, unmodified)", "tables": {}, "sieve": {}}
     sets = {"odd32": odd_primes(32), "odd64": odd_primes(64), "odd128": odd_primes(128),
             "odd256": odd_primes(256), "default96": default_primes()}
     rsets = {}
     for name, P in sets.items():
+        if only:
+            rsets[name] = ref.RefSet.build(P)
+            continue
         t0 = time.time()
         s = ref.RefSet.build(P)
         rsets[name] = s
@@ -74,6 +105,17 @@ def main():
                                 **stats_json(st, sets.get(setname, [11]), with_surv))
         print(name, st.pairs_tested, f"{time.time() - t0:.1f}s", flush=True)
 
+    if only:
+        if "C5" in only:
+            # BASELINE config 5, the headline: 10^5 < p <= 3*10^5 against the
+            # 256-prime set, whole range (engine.hpp:259-277, sievetable.hpp:199-205)
+            tri("C5", "odd256", 100001, 300000, with_surv=True)
+        if "C4S" in only:
+            c4_subsample(g, rsets["odd128"], sets["odd128"])
+        with open(out, "w") as f:
+            json.dump(g, f, indent=1, sort_keys=True)
+        print("updated", out, only)
+        return
     tri("C1", "odd32", 2, 2000, with_surv=True)
     tri("C3", "odd64", 2, 10000)
     tri("C5_sub", "odd256", 200001, 201000)
@@ -103,4 +145,4 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    main(tuple(sys.argv[1:]))

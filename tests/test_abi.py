@@ -106,6 +106,21 @@ def test_no_cpu_fallback_without_gpu():
         cuboid.SieveSet.build(odd_primes(4))
 
 
+def test_multi_gpu_refuses_without_gpu():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is visible")
+    m = C.c_void_p()
+    assert N.lib().cgpu_multi_create(2, None, C.byref(m)) == N.ERR_NO_DEVICE
+    assert not m.value
+
+
+def test_multi_null_handles_are_errors():
+    assert N.lib().cgpu_multi_sieve(None, 2, 0, 10, 0, N.TRIANGLE, None, None, None, 0, None, 0) == N.ERR_INVALID
+    assert N.lib().cgpu_multi_tables_load(None, None, 0, None, 0) == N.ERR_INVALID
+    assert N.lib().cgpu_multi_destroy(None) == N.OK
+
+
 def test_null_context_is_an_error():
     assert N.lib().cgpu_sieve_launch(None, 2, 0, 10, N.TRIANGLE, 1, 0, 0) == N.ERR_INVALID
     assert N.lib().cgpu_destroy(None) == N.OK

@@ -16,7 +16,7 @@ from oracle import port
 from oracle import ref as refmod
 from paper_1601_00636_b200 import _native as N
 from paper_1601_00636_b200 import cuboid
-from paper_1601_00636_b200.device import Device
+from paper_1601_00636_b200.device import Device, serialize_index as device_serialize_index
 from paper_1601_00636_b200.primes import default_primes, odd_primes, primes_in_range
 
 pytestmark = pytest.mark.gpu
@@ -216,13 +216,15 @@ def test_random_ranges_vs_oracle(dev, seed):
             assert got == want
 
 
-@pytest.mark.parametrize("prime,flip", [(11, (2, 5)), (13, (0, 4)), (13, (7, 12))])
+@pytest.mark.parametrize("prime,flip", [(11, (2, 5)), (13, (0, 4)), (13, (7, 12)), (11, (0, 3))])
 def test_non_canonical_tables_vs_oracle(dev, prime, flip):
     """Tables loaded from bytes the reference's builder would never produce
     (one flipped bit of a row a >= 1, which breaks u(la, lb) = u(a, b), or of
-    row 0) must still sieve exactly like the reference's scan(): the kernel
-    reads the bits as loaded and, like engine.hpp:240-242, never probes row
-    0 (k_derive writes it as zeros)."""
+    row 0) must still sieve exactly like the reference itself (oracle/_ref,
+    the reference headers loaded with the same bytes): REGION never probes row
+    0 (scan(), engine.hpp:240-242), TRIANGLE reads it like any other row (the
+    is_unsolvable loop, sievetable.hpp:199-205) -- the context re-derives
+    its layout when a set with bits in row 0 switches mode."""
     P = odd_primes(96)
     tb, offs = port.build_set(P)
     k = P.index(prime)
@@ -232,12 +234,20 @@ def test_non_canonical_tables_vs_oracle(dev, prime, flip):
     bad[int(offs[k]) + (i >> 3)] ^= 1 << (i & 7)
     bad = bytes(bad)
     dev.load(P, bad)
-    for lo, hi, mode in ((2, 3000, N.TRIANGLE), (152, 700, N.REGION)):
+    rset = refmod.RefSet.load(bad, device_serialize_index(P))
+    for lo, hi, mode in ((2, 3000, N.TRIANGLE), (152, 700, N.REGION), (2, 1500, N.TRIANGLE)):
         o = port.sieve(bad, P, offs, lo, hi, mode)
         r = dev.sieve(lo, hi, mode, surv_cap=1 << 22)
         assert (r.pairs_tested, r.survivors) == (o["pairs_tested"], o["survivors"])
         assert r.hist.tolist() == o["hist"].tolist()
         assert np.array_equal(r.survivor_pairs, o["survivor_pairs"])
+        if mode == N.TRIANGLE:
+            w = refmod.triangle(rset, lo, hi, 4, with_sink=True)
+        else:
+            w = refmod.scan(rset, lo, 3, hi, with_sink=True)
+        assert (r.pairs_tested, r.survivors) == (w.pairs_tested, w.survivors)
+        assert r.hist.tolist() == list(w.hist_by_rank)
+        assert [tuple(x) for x in r.survivor_pairs.tolist()] == [(p, q) for p, q, _ in w.survivor_pairs]
 
 
 REG_LAYOUTS = [
@@ -363,41 +373,43 @@ def test_block_cyclic_shards_merge_to_full(dev, golden, sets, G):
 
 # ---- BASELINE full sizes: size-independent properties ------------------------------------
 
-def test_c5_full_range_properties(dev, golden, sets):
-    """C5 (10^5 < p <= 3*10^5, 256 primes, 2.43e10 pairs): pairs = sum phi(p);
-    every pair is killed or survives; 4-way block-cyclic shards merge to the
-    full result; the reference-checked 1000-row sub-range agrees."""
+def test_c5_full_range_vs_reference(dev, golden, sets):
+    """C5, the headline config (10^5 < p <= 3*10^5, 256 primes, 2.43e10 pairs)
+    over its WHOLE range against the reference's own result (golden C5 from
+    oracle/_ref: engine.hpp:259-277 statistics with sievetable.hpp:199-205
+    probes): pairs, survivors, the first-killer histogram and all 2001 block
+    r_max values; plus 4-way block-cyclic shards merging to it."""
     s = _set(sets, "odd256")
     full = cuboid.scan_triangle(s, 100001, 300000)
+    g = golden["sieve"]["C5"]
+    assert (g["p_lo"], g["p_hi"], g["set"]) == (100001, 300000, "odd256")
+    _check(full, g, sets["odd256"])
     assert full.pairs_tested == phi_sum(100001, 300000) == 24317097730
-    assert full.histogram_total() + full.survivors == full.pairs_tested
     merged = cuboid.ScanStats()
     for k in range(4):
         merged.merge(cuboid.scan_triangle(s, 100001, 300000, shard=(4, k)))
-    assert (merged.pairs_tested, merged.survivors, merged.kill_histogram, merged.block_r_max) == \
-        (full.pairs_tested, full.survivors, full.kill_histogram, full.block_r_max)
+    _check(merged, g, sets["odd256"])
     sub = cuboid.scan_triangle(s, 200001, 201000)
     _check(sub, golden["sieve"]["C5_sub"], sets["odd256"])
 
 
-def test_c4_random_subsample_classify(dev, sets):
-    """C4's seeded 10^6-pair subsample: first-killer rank of each
-    pair from the device classify path == the C oracle's rank-ordered probe."""
+def test_c4_random_subsample_classify(dev, golden, sets):
+    """C4's seeded 10^6-pair subsample (p weighted by phi(p), q
+    uniform among the coprime residues, tests/subsample.py): the first-killer
+    rank of every pair from the device classify path equals the reference's
+    rank-ordered SieveSet::is_unsolvable (golden C4_subsample, oracle/_ref)."""
+    import subsample
+    g = golden["sieve"]["C4_subsample"]
     P = sets["odd128"]
     tb, offs = port.build_set(P)
     dev.load(P, tb)
-    rng = np.random.default_rng(20160401)
-    p = rng.integers(2, 100001, 10**6, dtype=np.uint64)
-    q = (rng.integers(0, 1 << 62, 10**6, dtype=np.uint64) % (p - 1)) + 1
-    got = dev.classify(np.stack([p, q], 1))
-    # oracle: same rank-ordered probe, vectorised over the packed bytes
-    want = np.full(len(p), -1, np.int64)
-    buf = np.frombuffer(tb, np.uint8)
-    for k, r in enumerate(P):
-        i = (p % r) * r + (q % r)
-        hit = ((buf[offs[k] + (i >> 3)] >> (i & 7).astype(np.uint8)) & 1).astype(bool)
-        want[(want < 0) & hit] = k
-    assert np.array_equal(got, want)
+    pq = subsample.sample(g["n"], g["seed"], g["p_max"])
+    assert hashlib.sha256(pq.tobytes()).hexdigest() == g["pairs_sha256"]
+    got = dev.classify(pq).astype("<i4")
+    assert hashlib.sha256(got.tobytes()).hexdigest() == g["ranks_sha256"]
+    hist = np.bincount(got + 1, minlength=len(P) + 1)
+    assert int(hist[0]) == g["survivors"]
+    assert {str(P[k]): int(c) for k, c in enumerate(hist[1:]) if c} == g["rank_histogram"]
 
 
 def test_sharded_sieve_single_rank(dev):
@@ -618,12 +630,20 @@ def test_build_is_deterministic(dev, sets):
 
 
 def test_verify_small_region_pin(golden):
-    """engine.hpp:609-640 / test_engine.cpp:416-423: 413,362 pairs, all sieved out."""
+    """engine.hpp:609-640 / test_engine.cpp:416-423: 413,362 pairs, all sieved
+    out; every survivor goes through the reference's own verify_pair(bypass)."""
     s = cuboid.SieveSet.build_default()
-    v = cuboid.verify_small_region(s)
+    rset = refmod.RefSet.build(default_primes())
+    v = cuboid.verify_small_region(s, lambda p, q: refmod.verify_pair(rset, p, q, True)[0])
     g = golden["verify_small_region"]
-    assert (v.pairs, v.sieved_out, v.survivors, v.candidates) == \
-        (g["pairs"], g["sieved_out"], g["survivors"], g["candidates"])
+    assert (v.pairs, v.sieved_out, v.survivors, v.no_integer_root, v.root_fails, v.candidates) == \
+        (g["pairs"], g["sieved_out"], g["survivors"], g["no_integer_root"], g["root_fails"],
+         g["candidates"])
     weak = cuboid.SieveSet.build([11])
-    w = cuboid.verify_small_region(weak)
-    assert w.survivors > 0 and w.survivors + w.sieved_out == w.pairs
+    wref = refmod.RefSet.build([11])
+    w = cuboid.verify_small_region(weak, lambda p, q: refmod.verify_pair(wref, p, q, True)[0])
+    want = refmod.verify_small_region(wref)
+    assert w.survivors > 0
+    assert vars(w) == want
+    with pytest.raises(TypeError):
+        cuboid.verify_small_region(weak, None)

@@ -15,6 +15,8 @@ from oracle import port
 from oracle import ref as refmod
 from paper_1601_00636_b200.primes import default_primes, is_prime, odd_primes, primes_in_range
 
+needs_ref_early = pytest.mark.skipif(not refmod.available(), reason="oracle/_ref not built")
+
 # proj/tests/test_sievetable.cpp:12-37 -- the 11x11 matrix U_11 of the paper's
 # Table 2.5 (rows p~, columns q~) and its 16 packed bytes (PAPER.md (2.6)).
 U11_BYTES = bytes.fromhex("00E09F7EEDED76CF7BDEEDF6D62FFF00")
@@ -235,6 +237,55 @@ def test_config_pins(golden):
     assert s["C3"]["pairs_tested"] == 30397485
     assert s["C4"]["pairs_tested"] == 3039650753 and s["C4"]["survivors"] == 0
     assert s["C5_sub"]["pairs_tested"] == 121858132
+
+
+def test_c5_golden_is_the_full_headline_range(golden):
+    """The headline config's reference result covers all of C5: 2.43e10 pairs
+    (sum phi(p)), 0 survivors, one r_max per p/100 block."""
+    g = golden["sieve"]["C5"]
+    assert (g["p_lo"], g["p_hi"], g["mode"], g["set"]) == (100001, 300000, "TRIANGLE", "odd256")
+    assert g["pairs_tested"] == 24317097730 and g["survivors"] == 0
+    assert sum(g["kill_histogram"].values()) == g["pairs_tested"]
+    assert len(g["block_r_max"]) == 300000 // 100 - 100001 // 100 + 1
+
+
+def test_c4_subsample_sampler_and_ranks(golden):
+    """The phi-weighted coprime sampler (tests/subsample.py) reproduces the
+    golden's pairs, and a numpy restatement of is_unsolvable's rank-ordered
+    probe (sievetable.hpp:199-205) over the C oracle's tables reproduces the
+    reference's first-killer ranks (oracle/_ref, golden C4_subsample)."""
+    import math
+
+    import subsample
+    g = golden["sieve"]["C4_subsample"]
+    pq = subsample.sample(g["n"], g["seed"], g["p_max"])
+    assert hashlib.sha256(pq.tobytes()).hexdigest() == g["pairs_sha256"]
+    p, q = pq[:, 0], pq[:, 1]
+    assert bool(np.all((q >= 1) & (q < p))) and bool(np.all(np.gcd(p, q) == 1))
+    assert all(math.gcd(int(a), int(b)) == 1 for a, b in pq[:100])
+    P = odd_primes(128)
+    tb, offs = port.build_set(P)
+    buf = np.frombuffer(tb, np.uint8)
+    ranks = np.full(len(p), -1, np.int32)
+    for k, r in enumerate(P):
+        i = (p % r) * r + (q % r)
+        hit = ((buf[offs[k] + (i >> 3)] >> (i & 7).astype(np.uint8)) & 1).astype(bool)
+        ranks[(ranks < 0) & hit] = k
+    assert hashlib.sha256(ranks.astype("<i4").tobytes()).hexdigest() == g["ranks_sha256"]
+
+
+@needs_ref_early
+def test_c4_subsample_ref_classify_spot(golden):
+    """The golden's ranks come from SieveSet::is_unsolvable: spot-check 2000
+    pairs through the reference library directly."""
+    import subsample
+    g = golden["sieve"]["C4_subsample"]
+    pq = subsample.sample(g["n"], g["seed"], g["p_max"])[:2000]
+    rs = refmod.RefSet.build(odd_primes(128))
+    got = refmod.classify(rs, pq, 2)
+    for (a, b), k in zip(pq[:50].tolist(), got[:50].tolist()):
+        want = next((j for j in range(128) if rs.is_unsolvable(j, a, b)), -1)
+        assert k == want
 
 
 def test_small_region_pin(golden):
