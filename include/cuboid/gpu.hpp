@@ -381,12 +381,13 @@ private:
 	uint64_t q_low_of(uint64_t p)
 	{
 		if (p < kRegionCrossover) return q_bounds(p).q_low;
-		if (c_ == 0) c_ = q_bounds(p).q_low;
+		if (c_ == 0 || p < last_p_) c_ = q_bounds(p).q_low;  // a walk restarted behind the last one
+		last_p_ = p;
 		while (9 * static_cast<unsigned __int128>(c_) * c_ * c_ < p) ++c_;  // least q with 9q^3 >= p
 		return c_;
 	}
 	uint64_t p_end_;
-	uint64_t c_ = 0;
+	uint64_t c_ = 0, last_p_ = 0;
 };
 
 inline void fold(const SieveSet& set, const DeviceScan& d, ScanStats& st, const ScanSink& sink)

@@ -97,8 +97,13 @@ def lib():
             raise ImportError(f"{LIB_PATH} not built: run __graft_entry__.build() "
                               "(make -C paper_1601_00636_b200)")
         L = C.CDLL(LIB_PATH)
+        variant = "CUBOID_GPU_LIB" in os.environ  # A/B tools load older builds too
         for name, (res, args) in SIGNATURES.items():
-            fn = getattr(L, name)
+            fn = getattr(L, name, None)
+            if fn is None and variant:
+                continue
+            if fn is None:
+                raise ImportError(f"{LIB_PATH} lacks {name}: rebuild it")
             fn.restype = res
             fn.argtypes = args
         _lib = L

@@ -637,7 +637,10 @@ __device__ __forceinline__ uint32_t dispatch_row(const SieveArgs& a, const WarpS
 __device__ unsigned long long g_wclk[3 * 8192];
 #endif
 
-template <int NR2, int NR3, bool STD>
+// STOP: polls the cooperative stop word (SieveArgs::stop). The standard-prime
+// kernel, the benchmarked one, also exists without the poll: even a per-row
+// test of a kernel parameter moved its code layout and cost it ~6% (C5).
+template <int NR2, int NR3, bool STD, bool STOP = true>
 __global__ void __launch_bounds__(kSieveThreads, kSieveMinBlocks) k_sieve(const SieveArgs a)
 {
 	constexpr int NREG = NR2 + NR3;
@@ -702,7 +705,8 @@ __global__ void __launch_bounds__(kSieveThreads, kSieveMinBlocks) k_sieve(const 
 		const unsigned long long u0 = ws - rs, u1 = min(we, re) - rs;
 		ws = min(we, re);
 		const uint32_t cur = slot++;
-		if (a.stop && (cur & 7u) == 0 && *a.stop) break;  // stop raised: abandon the launch
+		if constexpr (STOP)  // a stop raised: abandon the launch (the caller re-sieves exactly)
+			if (a.stop && (cur & 7u) == 0 && *a.stop) break;
 		const uint32_t rcost = a.row_cost;
 		if (u1 <= rcost) continue;
 		const RowBounds rb = slot_row(a, cur);
@@ -833,17 +837,18 @@ __global__ void k_classify(const uint64_t* __restrict__ pq, uint64_t n,
 	}
 }
 
-template <int NR2, int NR3, bool STD = false>
+template <int NR2, int NR3, bool STD = false, bool STOP = true>
 void* sieve_fn()
 {
-	return reinterpret_cast<void*>(&k_sieve<NR2, NR3, STD>);
+	return reinterpret_cast<void*>(&k_sieve<NR2, NR3, STD, STOP>);
 }
 
 // Instantiated: NR2 in 0..8 with NR3 = 0, and NR2 = 7 (every prime 11..31
-// killable -- all BASELINE sets) with NR3 in 1..kMaxReg3.
-void* sieve_kernel_ptr(int nr2, int nr3, bool std_primes)
+// killable -- all BASELINE sets) with NR3 in 1..kMaxReg3; the standard-prime
+// kernel with and without the stop poll.
+void* sieve_kernel_ptr(int nr2, int nr3, bool std_primes, bool stop = true)
 {
-	if (std_primes) return sieve_fn<7, 1, true>();
+	if (std_primes) return stop ? sieve_fn<7, 1, true, true>() : sieve_fn<7, 1, true, false>();
 	if (nr2 == 7 && nr3 > 0) {
 		switch (nr3) {
 		case 1: return sieve_fn<7, 1>();
@@ -883,10 +888,13 @@ int sieve_grid(int device, int nr2, int nr3, bool std_primes, size_t smem)
 	// per-launch-size attribute set for one would reject another's launch.
 	int optin = 0;
 	cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
-	cudaFuncAttributes fa{};
-	cudaFuncGetAttributes(&fa, fn);
-	cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-	                     optin - static_cast<int>(fa.sharedSizeBytes));
+	const void* variants[2] = {fn, sieve_kernel_ptr(nr2, nr3, std_primes, false)};
+	for (const void* f : variants) {
+		cudaFuncAttributes fa{};
+		cudaFuncGetAttributes(&fa, f);
+		cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
+		                     optin - static_cast<int>(fa.sharedSizeBytes));
+	}
 	cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kSieveThreads, smem);
 	if (per_sm < 1) per_sm = 1;
 	return sms * per_sm;
@@ -902,7 +910,8 @@ cudaError_t launch_sieve(const SieveArgs& a, int grid, cudaStream_t s)
 {
 	const size_t smem = sieve_smem_bytes(a.np, a.wtab_n ? (a.std_primes ? kTabStrideStd : kTabStrideGen) : 0);
 	void* args[] = {const_cast<SieveArgs*>(&a)};
-	return cudaLaunchKernel(sieve_kernel_ptr(static_cast<int>(a.nreg2), static_cast<int>(a.nreg3), a.std_primes),
+	return cudaLaunchKernel(sieve_kernel_ptr(static_cast<int>(a.nreg2), static_cast<int>(a.nreg3), a.std_primes,
+	                                         a.stop != nullptr),
 	                        dim3(grid),
 	                        dim3(kSieveThreads), args, smem, s);
 }
