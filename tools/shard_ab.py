@@ -26,11 +26,13 @@ c4 = best(2, 100000, k=4)
 print(json.dumps({"C5": full, "C5_shard4_worst": worst4, "eff4": full / 4 / worst4,
                   "C5_shard8_worst": worst8, "eff8": full / 8 / worst8, "C4": c4}))
 '''
-for spec in sys.argv[1].split(","):  # LIB or LIB@ALPHA (CUBOID_DRAIN_ALPHA)
-    lib, _, alpha = spec.partition("@")
+KNOBS = ("CUBOID_DRAIN_ALPHA", "CUBOID_POOL_FRAC", "CUBOID_POOL_DIV", "CUBOID_ROW_COST")
+for spec in sys.argv[1].split(","):  # LIB[@ALPHA[@POOL_FRAC[@POOL_DIV[@ROW_COST]]]] (empty = default)
+    lib, *knobs = spec.split("@")
     env = dict(os.environ, ROOT=ROOT)
-    if alpha:
-        env["CUBOID_DRAIN_ALPHA"] = alpha
+    for name, v in zip(KNOBS, knobs):
+        if v:
+            env[name] = v
     if lib != "default":
         env["CUBOID_GPU_LIB"] = os.path.join(ROOT, lib)
     r = subprocess.run([sys.executable, "-c", CHILD], env=env, capture_output=True, text=True)
