@@ -458,10 +458,11 @@ def run_ours(args, wl, primes):
     # and the others hold 0 (k_init_blocks). Each rank writes its survivors
     # into its own slice of a zeroed region, so the SUM is the gather.
     n_acc, n_surv = 2 + n, world * GATHER_CAP
-    buf = torch.zeros(n_acc + nblocks + n_surv, dtype=torch.int64, device=cuda)
+    # + 1 slot: the asynchronous table load's status word (e2e steps; 0 = verified)
+    buf = torch.zeros(n_acc + nblocks + n_surv + 1, dtype=torch.int64, device=cuda)
     acc = buf[:n_acc]
     brm_sum = buf[n_acc:n_acc + nblocks]
-    surv_all = buf[n_acc + nblocks:]
+    surv_all = buf[n_acc + nblocks:n_acc + nblocks + n_surv]
     brm = torch.zeros(nblocks, dtype=torch.int32, device=cuda)  # the kernel writes u32 r_max
     surv_mine = surv_all[g * GATHER_CAP:(g + 1) * GATHER_CAP]
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=cuda)  # > 126 MB L2
@@ -534,13 +535,16 @@ def run_ours(args, wl, primes):
         def issue(self):
             b = self.buf
             with torch.cuda.stream(self.stream):
+                # asynchronous loads: no host wait inside the step; the load is
+                # verified on the device and its status word rides in the result
+                # vector (checked below)
                 if world > 1:  # 1/G of the bytes per rank over PCIe, all-gathered over NVLink
-                    self.full = parallel.load_tables_sharded(self.dev, pr, pinned)
+                    self.full = parallel.load_tables_sharded(self.dev, pr, pinned, async_=True)
                 else:
-                    N.check(L.cgpu_tables_load(self.dev._ctx, pr.ctypes.data_as(C.c_void_p), n,
-                                               C.c_void_p(pinned.data_ptr()), len(tables)))
-                if world > 1:
+                    self.dev.load_host_async(pr, pinned.data_ptr(), len(tables))
+                if world > 1:  # survivor slices and the status slot are summed over ranks
                     b[n_acc + nblocks:].zero_()
+                self.dev.load_status_copy(b[-1:].data_ptr())
                 N.check(L.cgpu_sieve_launch_dev(
                     self.dev._ctx, wl["p_lo"], 0, wl["p_hi"], N.TRIANGLE, G, g,
                     C.c_void_p(b.data_ptr()), C.c_void_p(b.data_ptr() + 16), C.c_void_p(self.brm.data_ptr()),
@@ -576,9 +580,11 @@ def run_ours(args, wl, primes):
     e2e_total = allreduce_max(float(np.sum(e2e_s)))
     clk.__exit__()
     e2e_res = h_buf.numpy()
+    load_status = int(e2e_res[-1])  # summed over ranks: 0 iff every rank's asynchronous load verified
     e2e_parity = golden_parity(args.workload, primes, int(e2e_res[0]), int(e2e_res[1]),
                                e2e_res[2:n_acc], e2e_res[n_acc:n_acc + nblocks], wl)
-    parity_ok = parity_ok and e2e_parity["ok"]
+    parity_ok = parity_ok and e2e_parity["ok"] and load_status == 0
+    e2e_parity["load_status"] = load_status
 
     # ---- roofline of the dominant kernel (k_sieve), rank-local ------------------------------
     if world > 1:  # this rank's own pairs for the per-launch figure
@@ -668,13 +674,16 @@ def run_ours(args, wl, primes):
                                       "all-reduce(SUM) of counts/histogram/block r_max/survivor slices"},
             "parity": "ok" if parity_ok else "MISMATCH",
             "parity_detail": parity,
+            "parity_detail_e2e": e2e_parity,
             "e2e": {"value": pairs * args.steps / e2e_total, "unit": "pairs/s",
                     "h2d_bytes_per_step": (parallel.table_slice(len(tables), world, 0)[2] if world > 1
                                            else len(tables)) + 4 * n,
                     "d2h_bytes_per_step": 8 * buf.numel(),
                     "ms_per_step": 1e3 * e2e_total / args.steps,
-                    "path": "per step: cgpu_tables_load(pinned host tables) + cgpu_sieve_launch_dev + "
-                            "reduce + D2H of the result vector; two contexts/streams pipelined 2 deep "
+                    "path": "per step: cgpu_tables_load_async(pinned host tables; no host wait, "
+                            "verified on the device, status word in the result vector) + "
+                            "cgpu_sieve_launch_dev + reduce + D2H of the result vector; two "
+                            "contexts/streams pipelined 2 deep "
                             "(step i+1's upload overlaps step i's sieve); at N>1 each rank uploads "
                             "1/N of the tables (h2d bytes are per rank) and one all-gather assembles "
                             "the set (parallel.load_tables_sharded, cgpu_tables_load_dev)"},

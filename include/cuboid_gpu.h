@@ -107,6 +107,27 @@ int cgpu_tables_load(cgpu_ctx* ctx, const uint32_t* primes, uint32_t n, const ui
 int cgpu_tables_load_dev(cgpu_ctx* ctx, const uint32_t* primes, uint32_t n, const void* d_bytes,
                          uint64_t nbytes);
 
+/* Asynchronous loads, for pipelines that upload a set every step (the e2e
+ * bench, the multi-GPU sharded upload): as cgpu_tables_load /
+ * cgpu_tables_load_dev, but nothing waits for the device. The probe list is
+ * built from the EXPECTED per-table flags (those last verified for the same
+ * prime list on this context, else the reference builder's: every table of
+ * r >= 11 has a set bit, r <= 7 none) and a device check compares them with
+ * the derived ones. The bytes must stay valid until the stream has consumed
+ * them. Errors surface later: cgpu_load_status (waits) returns the deferred
+ * FormatError (nonzero padding) or CGPU_ERR_INVALID if the flags differed
+ * (the context then re-derives; launches made since the load must be
+ * repeated); cgpu_sieve_results and cgpu_tables_info check it too.
+ * cgpu_load_status_copy enqueues a copy of the 32-bit status word (0 = ok,
+ * bit 0 padding error, bit 1 flag mismatch) to dst (device or pinned host
+ * memory) on the context stream, for callers that never synchronise. */
+int cgpu_tables_load_async(cgpu_ctx* ctx, const uint32_t* primes, uint32_t n, const uint8_t* bytes,
+                           uint64_t nbytes);
+int cgpu_tables_load_dev_async(cgpu_ctx* ctx, const uint32_t* primes, uint32_t n, const void* d_bytes,
+                               uint64_t nbytes);
+int cgpu_load_status(cgpu_ctx* ctx);
+int cgpu_load_status_copy(cgpu_ctx* ctx, void* dst);
+
 /* Copies the resident packed tables back (total_bytes) -- byte-identical to
  * serialize_tables (sievetable.hpp:229). */
 int cgpu_tables_download(cgpu_ctx* ctx, uint8_t* out_bytes, uint64_t cap);

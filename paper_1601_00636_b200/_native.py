@@ -36,6 +36,10 @@ SIGNATURES = {
                                     C.c_void_p, _u64p]),
     "cgpu_tables_load": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint32, C.c_void_p, C.c_uint64]),
     "cgpu_tables_load_dev": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint32, C.c_void_p, C.c_uint64]),
+    "cgpu_tables_load_async": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint32, C.c_void_p, C.c_uint64]),
+    "cgpu_tables_load_dev_async": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint32, C.c_void_p, C.c_uint64]),
+    "cgpu_load_status": (C.c_int, [C.c_void_p]),
+    "cgpu_load_status_copy": (C.c_int, [C.c_void_p, C.c_void_p]),
     "cgpu_tables_download": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64]),
     "cgpu_tables_info": (C.c_int, [C.c_void_p, _u32p, C.c_void_p]),
     "cgpu_build_tables": (C.c_int, [C.c_int, C.c_void_p, C.c_uint32, C.c_int, C.c_void_p,

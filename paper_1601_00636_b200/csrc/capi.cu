@@ -139,6 +139,15 @@ struct cgpu_ctx {
 	// skips those primes, engine.hpp:240-242), as loaded for TRIANGLE when a
 	// non-canonical set has bits there (is_unsolvable reads it)
 	bool keep_row0 = false, row0_nonzero = false;
+	// asynchronous (speculative) loads: the per-table flags the probe list was
+	// built from, the last verified flags of a prime list, and the device word
+	// k_load_check writes (padding error | flag mismatch << 1)
+	std::vector<uint32_t> flags_primes;
+	std::vector<uint8_t> flags;
+	std::vector<uint8_t> spec_flags;
+	bool flags_valid = false, status_pending = false;
+	DevBuf<uint8_t> d_expect;
+	DevBuf<uint32_t> load_status;
 	uint64_t total_bytes = 0, ext_words = 0;
 	DevBuf<uint8_t> packed;
 	DevBuf<uint32_t> ext, d_primes, d_offsets, killflags;
@@ -311,7 +320,8 @@ std::vector<PrimeJob> make_jobs(const std::vector<uint32_t>& primes,
 // build the probe list (killable tables in rank order).
 // check_padding: a k_check_padding flag was enqueued into killflags[n]; it
 // is read back with the killable flags (one host sync per load).
-int finalize_set(cgpu_ctx* c, bool check_padding = false, bool keep_row0 = false)
+int finalize_set(cgpu_ctx* c, bool check_padding = false, bool keep_row0 = false,
+                 const std::vector<uint8_t>* spec = nullptr)
 {
 	const uint32_t n = static_cast<uint32_t>(c->primes.size());
 	std::vector<PrimeJob> jobs = make_jobs(c->primes, c->offsets, c->ext_base, c->ext_words);
@@ -338,10 +348,31 @@ int finalize_set(cgpu_ctx* c, bool check_padding = false, bool keep_row0 = false
 		++c->launches;
 	}
 	std::vector<uint32_t> kf(n + 1, 0);
-	const uint32_t nread = n + (check_padding ? 1 : 0);
-	if (nread) CK(cudaMemcpyAsync(kf.data(), c->killflags.p, 4ull * nread, cudaMemcpyDeviceToHost, c->stream));
-	CK(cudaStreamSynchronize(c->stream));
-	if (check_padding && kf[n]) return set_err(CGPU_ERR_FORMAT, "unpack_bits: nonzero padding bits");
+	if (spec) {  // asynchronous load: build from the expected flags, verify on the device
+		for (uint32_t k = 0; k < n; ++k) kf[k] = (*spec)[k];
+		CK(c->d_expect.ensure(n));
+		CK(c->load_status.ensure(1));
+		if (n) {
+			CK(cudaMemcpyAsync(c->d_expect.p, spec->data(), n, cudaMemcpyHostToDevice, c->stream));
+			if (!check_padding) CK(cudaMemsetAsync(c->killflags.p + n, 0, 4, c->stream));
+			CK(launch_load_check(c->killflags.p, c->d_expect.p, n, c->load_status.p, c->stream));
+			++c->launches;
+		} else {
+			CK(cudaMemsetAsync(c->load_status.p, 0, 4, c->stream));
+		}
+		c->status_pending = true;
+		c->spec_flags = *spec;
+	} else {
+		const uint32_t nread = n + (check_padding ? 1 : 0);
+		if (nread) CK(cudaMemcpyAsync(kf.data(), c->killflags.p, 4ull * nread, cudaMemcpyDeviceToHost, c->stream));
+		CK(cudaStreamSynchronize(c->stream));
+		if (check_padding && kf[n]) return set_err(CGPU_ERR_FORMAT, "unpack_bits: nonzero padding bits");
+		c->status_pending = false;
+		c->flags_primes = c->primes;
+		c->flags.assign(n, 0);
+		for (uint32_t k = 0; k < n; ++k) c->flags[k] = static_cast<uint8_t>(kf[k] & 3u);
+		c->flags_valid = true;
+	}
 	c->killable.assign(n, 0);
 	c->probe_rank.clear();
 	c->probe_r.clear();
@@ -438,9 +469,49 @@ int finalize_set(cgpu_ctx* c, bool check_padding = false, bool keep_row0 = false
 		c->grid = it->second;
 	}
 	CK(cudaGetLastError());
-	CK(cudaStreamSynchronize(c->stream));
+	if (!spec) CK(cudaStreamSynchronize(c->stream));
 	c->loaded = true;
 	c->launched = false;
+	return CGPU_OK;
+}
+
+// The expected per-table flags of an asynchronous load: the verified flags of
+// the same prime list when this context has them (a set re-uploaded, e.g.
+// every step of a pipeline), else what the reference's builder produces --
+// every table of r >= 11 has a set bit, r = 2, 3, 5, 7 none, no row 0 bits.
+std::vector<uint8_t> expected_flags(const cgpu_ctx* c, const std::vector<uint32_t>& primes)
+{
+	if (c->flags_valid && c->flags_primes == primes) return c->flags;
+	std::vector<uint8_t> f(primes.size());
+	for (size_t k = 0; k < primes.size(); ++k) f[k] = primes[k] > 7 ? 1 : 0;
+	return f;
+}
+
+// Verifies the last asynchronous load (waits for the stream). On a flag
+// mismatch the context re-derives synchronously, so later launches are right;
+// launches made before the verification used the wrong probe list.
+int settle_load(cgpu_ctx* c)
+{
+	if (!c->status_pending) return CGPU_OK;
+	uint32_t st = 0;
+	CK(cudaMemcpyAsync(&st, c->load_status.p, 4, cudaMemcpyDeviceToHost, c->stream));
+	CK(cudaStreamSynchronize(c->stream));
+	c->status_pending = false;
+	if (st & 1u) {
+		c->loaded = false;
+		return set_err(CGPU_ERR_FORMAT, "unpack_bits: nonzero padding bits");
+	}
+	if (st & 2u) {
+		c->flags_valid = false;
+		if (int rc = finalize_set(c, false, c->keep_row0)) return rc;
+		return set_err(CGPU_ERR_INVALID,
+		               "asynchronous load: the tables' flags differ from the expected ones; the set was "
+		               "re-derived, repeat the launches made since the load");
+	}
+	// verified: remember the flags for the next load of this prime list
+	c->flags_primes = c->primes;
+	c->flags = c->spec_flags;
+	c->flags_valid = true;
 	return CGPU_OK;
 }
 
@@ -522,7 +593,7 @@ int cgpu_tables_build(cgpu_ctx* c, const uint32_t* primes, uint32_t n, int algor
 }
 
 static int tables_load(cgpu_ctx* c, const uint32_t* primes, uint32_t n, const void* bytes, uint64_t nbytes,
-                       cudaMemcpyKind kind);
+                       cudaMemcpyKind kind, bool async = false);
 
 int cgpu_tables_load(cgpu_ctx* c, const uint32_t* primes, uint32_t n, const uint8_t* bytes,
                      uint64_t nbytes)
@@ -536,8 +607,39 @@ int cgpu_tables_load_dev(cgpu_ctx* c, const uint32_t* primes, uint32_t n, const 
 	return tables_load(c, primes, n, d_bytes, nbytes, cudaMemcpyDeviceToDevice);
 }
 
+int cgpu_tables_load_async(cgpu_ctx* c, const uint32_t* primes, uint32_t n, const uint8_t* bytes,
+                           uint64_t nbytes)
+{
+	return tables_load(c, primes, n, bytes, nbytes, cudaMemcpyHostToDevice, true);
+}
+
+int cgpu_tables_load_dev_async(cgpu_ctx* c, const uint32_t* primes, uint32_t n, const void* d_bytes,
+                               uint64_t nbytes)
+{
+	return tables_load(c, primes, n, d_bytes, nbytes, cudaMemcpyDeviceToDevice, true);
+}
+
+int cgpu_load_status(cgpu_ctx* c)
+{
+	if (!c) return set_err(CGPU_ERR_INVALID, "null ctx");
+	CK(cudaSetDevice(c->device));
+	return settle_load(c);
+}
+
+int cgpu_load_status_copy(cgpu_ctx* c, void* dst)
+{
+	if (!c || !dst) return set_err(CGPU_ERR_INVALID, "null argument");
+	CK(cudaSetDevice(c->device));
+	if (c->status_pending) {
+		CK(cudaMemcpyAsync(dst, c->load_status.p, 4, cudaMemcpyDefault, c->stream));
+	} else {
+		CK(cudaMemsetAsync(dst, 0, 4, c->stream));  // verified (or synchronous) load
+	}
+	return CGPU_OK;
+}
+
 static int tables_load(cgpu_ctx* c, const uint32_t* primes, uint32_t n, const void* bytes, uint64_t nbytes,
-                       cudaMemcpyKind kind)
+                       cudaMemcpyKind kind, bool async)
 {
 	if (!c) return set_err(CGPU_ERR_INVALID, "null ctx");
 	CK(cudaSetDevice(c->device));
@@ -559,6 +661,10 @@ static int tables_load(cgpu_ctx* c, const uint32_t* primes, uint32_t n, const vo
 		CK(cudaMemsetAsync(c->killflags.p + n, 0, 4, c->stream));
 		CK(launch_check_padding(c->jobs_rank.p, n, c->packed.p, c->killflags.p + n, c->stream));
 		++c->launches;
+	}
+	if (async) {
+		const std::vector<uint8_t> spec = expected_flags(c, c->primes);
+		return finalize_set(c, n > 0, false, &spec);
 	}
 	return finalize_set(c, n > 0);
 }
@@ -695,6 +801,10 @@ int cgpu_tables_save_files(cgpu_ctx* c, const char* tables_path, const char* ind
 int cgpu_tables_info(cgpu_ctx* c, uint32_t* n, uint8_t* killable)
 {
 	if (!c) return set_err(CGPU_ERR_INVALID, "null ctx");
+	if (c->status_pending) {
+		CK(cudaSetDevice(c->device));
+		if (int rc = settle_load(c)) return rc;
+	}
 	const uint32_t k = c->loaded ? static_cast<uint32_t>(c->primes.size()) : 0;
 	if (n) *n = k;
 	if (killable && k) std::memcpy(killable, c->killable.data(), k);
@@ -980,6 +1090,7 @@ int cgpu_sieve_results(cgpu_ctx* c, uint64_t* counts, uint64_t* hist, uint32_t* 
 	if (!c->launched || !c->results_internal)
 		return set_err(CGPU_ERR_INVALID, "no sieve launched into context buffers");
 	CK(cudaSetDevice(c->device));
+	if (int rc = settle_load(c)) return rc;  // an asynchronous load is verified here at the latest
 	unsigned long long cnt[2] = {0, 0};
 	std::vector<unsigned long long> hp(c->primes.size());
 	CK(cudaMemcpyAsync(cnt, c->counters.p, 16, cudaMemcpyDeviceToHost, c->stream));

@@ -42,6 +42,9 @@ cudaError_t launch_permute(const PrimeJob* d_jobs, uint32_t njobs, uint32_t max_
 cudaError_t launch_wintab(const uint4* d_probes, uint32_t nprobes, uint32_t entries, const uint32_t* d_ext,
                           uint32_t stride, uint32_t* d_out, cudaStream_t s);
 
+// Speculative-load check (k_load_check): *d_status = padding error | flag mismatch << 1.
+cudaError_t launch_load_check(const uint32_t* d_kf, const uint8_t* d_expect, uint32_t n, uint32_t* d_status,
+                              cudaStream_t s);
 cudaError_t launch_derive(const PrimeJob* d_jobs, const uint4* d_items, uint32_t nitems, const uint8_t* d_packed,
                           uint32_t* d_ext, uint32_t* d_killable, int keep_row0, cudaStream_t s);
 // k_derive work items {job, first row, rows, 0} of <= kDeriveItemWords output words each

@@ -452,6 +452,20 @@ __global__ void k_check_padding(const PrimeJob* __restrict__ jobs, uint32_t njob
 	}
 }
 
+// Verification of a speculative (asynchronous) load: the derive's per-table
+// flags (bit 0 killable, bit 1 row 0 has a set bit) against the ones the host
+// built the probe list from, and the padding check's flag at kf[n].
+// *status = padding error (1) | flag mismatch (2); the host reads it later.
+__global__ void k_load_check(const uint32_t* __restrict__ kf, const uint8_t* __restrict__ expect, uint32_t n,
+                             uint32_t* __restrict__ status)
+{
+	uint32_t bad = 0;
+	for (uint32_t k = threadIdx.x; k < n; k += blockDim.x)
+		if ((kf[k] & 3u) != expect[k]) bad = 2;
+	bad = __syncthreads_or(bad) ? 2u : 0u;
+	if (threadIdx.x == 0) *status = bad | (kf[n] ? 1u : 0u);
+}
+
 uint32_t grid_x(uint64_t units, uint32_t per_cta, uint32_t cap)
 {
 	const uint64_t x = (units + per_cta - 1) / per_cta;
@@ -546,6 +560,13 @@ std::vector<uint4> derive_items(const std::vector<uint32_t>& primes)
 		for (uint32_t a = 0; a < r; a += R) items.push_back(make_uint4(k, a, std::min(R, r - a), 0));
 	}
 	return items;
+}
+
+cudaError_t launch_load_check(const uint32_t* d_kf, const uint8_t* d_expect, uint32_t n, uint32_t* d_status,
+                              cudaStream_t s)
+{
+	k_load_check<<<1, 256, 0, s>>>(d_kf, d_expect, n, d_status);
+	return cudaGetLastError();
 }
 
 cudaError_t launch_check_padding(const PrimeJob* d_jobs, uint32_t njobs, const uint8_t* d_packed,

@@ -84,13 +84,32 @@ class Device:
         self.primes = pr.copy()
         self.offsets, self.total_bytes = self.layout(pr)
 
-    def load_dev(self, primes, d_ptr: int, nbytes: int):
+    def load_dev(self, primes, d_ptr: int, nbytes: int, async_: bool = False):
         """Upload packed tables that already sit in device memory on this GPU
-        (e.g. all-gathered by parallel.load_tables_sharded), on this stream."""
+        (e.g. all-gathered by parallel.load_tables_sharded), on this stream.
+        async_: cgpu_tables_load_dev_async (no host wait; verified later by
+        load_status / load_status_copy / the next results call)."""
         pr = np.ascontiguousarray(primes, dtype=np.uint32)
-        N.check(N.lib().cgpu_tables_load_dev(self._ctx, _ptr(pr), len(pr), C.c_void_p(d_ptr), int(nbytes)))
+        fn = N.lib().cgpu_tables_load_dev_async if async_ else N.lib().cgpu_tables_load_dev
+        N.check(fn(self._ctx, _ptr(pr), len(pr), C.c_void_p(d_ptr), int(nbytes)))
         self.primes = pr.copy()
         self.offsets, self.total_bytes = self.layout(pr)
+
+    def load_host_async(self, primes, h_ptr: int, nbytes: int):
+        """cgpu_tables_load_async from host memory at h_ptr (pinned for a truly
+        asynchronous copy; it must stay valid until the stream has read it)."""
+        pr = np.ascontiguousarray(primes, dtype=np.uint32)
+        N.check(N.lib().cgpu_tables_load_async(self._ctx, _ptr(pr), len(pr), C.c_void_p(h_ptr), int(nbytes)))
+        self.primes = pr.copy()
+        self.offsets, self.total_bytes = self.layout(pr)
+
+    def load_status(self):
+        """Verify the last asynchronous load (waits; raises on a deferred error)."""
+        N.check(N.lib().cgpu_load_status(self._ctx))
+
+    def load_status_copy(self, dst_ptr: int):
+        """Enqueue a copy of the load-status word (u32, 0 = ok) to dst_ptr."""
+        N.check(N.lib().cgpu_load_status_copy(self._ctx, C.c_void_p(dst_ptr)))
 
     def save_files(self, tables_path: str, index_path: str):
         """save_sieve_files of the resident set (sievetable.hpp:334-339)."""

@@ -154,18 +154,19 @@ def allgather_tables(host, device=None, group=None):
     return full[:total]
 
 
-def load_tables_sharded(dev, primes, host, group=None):
+def load_tables_sharded(dev, primes, host, group=None, async_=False):
     """Make the host table set resident on every rank's GPU through
     allgather_tables (1/G of the bytes over each rank's PCIe link), then load
     it from device memory (cgpu_tables_load_dev: padding check, device
     layouts) on torch's current stream, which must be the context's stream.
+    async_: the asynchronous load (no host wait; check dev.load_status_copy).
     Returns the gathered tensor (keep it alive until the stream has run)."""
     import torch
     import torch.distributed as dist
     pr = np.ascontiguousarray(primes, dtype=np.uint32)
     full = allgather_tables(host, torch.device("cuda", dev.device), group)
     if full.is_cuda:
-        dev.load_dev(pr, full.data_ptr(), full.numel())
+        dev.load_dev(pr, full.data_ptr(), full.numel(), async_=async_)
     else:
         dev.load(pr, full.numpy().tobytes())
     return full

@@ -471,6 +471,68 @@ def test_load_from_device_memory_and_nccl_sharded_upload(dev, golden, sets):
         dist.destroy_process_group()
 
 
+def test_async_loads_verified_on_the_device(dev, golden, sets):
+    """cgpu_tables_load_async / _dev_async (the e2e pipeline's loads, no host
+    wait): results identical to the reference's; a padding error and
+    non-canonical flags (an all-zero table the probe list expected to kill,
+    a set bit in row 0) are reported by the deferred status -- through the
+    status word, load_status and the next results call -- and the context
+    re-derives so the repeated launch is right."""
+    import torch
+    P = sets["odd64"]
+    tb, offs = port.build_set(P)
+    g = golden["sieve"]["C3"]
+    host = torch.frombuffer(bytearray(tb), dtype=torch.uint8).pin_memory()
+    word = torch.zeros(1, dtype=torch.int32).pin_memory()
+    for _ in range(3):  # first load speculates the builder's flags, later ones the verified flags
+        dev.load_host_async(P, host.data_ptr(), len(tb))
+        dev.load_status_copy(word.data_ptr())
+        r = dev.sieve(2, 10000, N.TRIANGLE)
+        assert int(word[0]) == 0
+        assert r.pairs_tested == g["pairs_tested"] and r.survivors == g["survivors"]
+        assert {str(P[k]): int(c) for k, c in enumerate(r.hist) if c} == g["kill_histogram"]
+    dev.load_status()
+    # a padding bit: FormatError at the status check
+    bad = bytearray(tb)
+    k11 = list(P).index(11)
+    bad[int(offs[k11]) + (11 * 11 + 7) // 8 - 1] |= 0x80
+    hb = torch.frombuffer(bad, dtype=torch.uint8).pin_memory()
+    dev.load_host_async(P, hb.data_ptr(), len(tb))
+    dev.load_status_copy(word.data_ptr())
+    with pytest.raises(N.CudaSieveError) as e:
+        dev.load_status()
+    assert e.value.code == N.ERR_FORMAT and int(word[0]) & 1
+    # the r = 11 table zeroed (never kills), against verified flags that say it kills
+    dev.load(P, tb)
+    z = bytearray(tb)
+    z[int(offs[k11]):int(offs[k11]) + (11 * 11 + 7) // 8] = bytes((11 * 11 + 7) // 8)
+    hz = torch.frombuffer(z, dtype=torch.uint8).pin_memory()
+    dev.load_host_async(P, hz.data_ptr(), len(tb))
+    dev.load_status_copy(word.data_ptr())
+    dev.synchronize()
+    assert int(word[0]) & 2
+    with pytest.raises(N.CudaSieveError) as e:
+        dev.sieve(2, 3000, N.TRIANGLE)  # the results call verifies the load
+    assert e.value.code == N.ERR_INVALID
+    r = dev.sieve(2, 3000, N.TRIANGLE)  # re-derived: right now
+    o = port.sieve(bytes(z), P, offs, 2, 3000, port.TRIANGLE)
+    assert (r.pairs_tested, r.survivors) == (o["pairs_tested"], o["survivors"])
+    assert r.hist.tolist() == o["hist"].tolist()
+    # a set bit in row 0 of r = 13: speculated canonical, reported, then exact in TRIANGLE
+    k13 = list(P).index(13)
+    w0 = bytearray(tb)
+    w0[int(offs[k13])] |= 0x10
+    h0 = torch.frombuffer(w0, dtype=torch.uint8).pin_memory()
+    dev.load(P, tb)
+    dev.load_host_async(P, h0.data_ptr(), len(tb))
+    with pytest.raises(N.CudaSieveError):
+        dev.load_status()
+    r = dev.sieve(2, 3000, N.TRIANGLE)
+    o = port.sieve(bytes(w0), P, offs, 2, 3000, port.TRIANGLE)
+    assert (r.pairs_tested, r.survivors) == (o["pairs_tested"], o["survivors"])
+    assert r.hist.tolist() == o["hist"].tolist()
+
+
 def test_files_roundtrip_with_reference(tmp_path, sets):
     """GPU-built tables written through the C ABI are the reference's files
     (save_sieve_files / load_sieve_files, test_sievetable.cpp:240-262), and
