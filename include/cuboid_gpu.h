@@ -303,6 +303,13 @@ int cgpu_multi_last_ms(cgpu_multi* m, float* ms);
 /* q_bounds (region.hpp:49-63). */
 int cgpu_q_bounds(uint64_t p, uint64_t* q_low, uint64_t* q_high);
 
+/* The pair k steps after (p, q) in the order scan() visits q (rows p,
+ * q_low(p)..q_high(p); the first row from q, engine.hpp:225-247), counting
+ * every q (skipped pairs too, as the stop-poll counter does, :248). CGPU_OK
+ * with *out_p, *out_q, or CGPU_P_ABOVE_LIMIT (3) if row p_end ends first.
+ * Host-only; O(rows). */
+int cgpu_region_advance(uint64_t p, uint64_t q, uint64_t k, uint64_t p_end, uint64_t* out_p, uint64_t* out_q);
+
 #ifdef __cplusplus
 }
 #endif

@@ -82,6 +82,7 @@ SIGNATURES = {
     "cgpu_last_launch_count": (C.c_int, [C.c_void_p, _u32p]),
     "cgpu_classify": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p]),
     "cgpu_q_bounds": (C.c_int, [C.c_uint64, _u64p, _u64p]),
+    "cgpu_region_advance": (C.c_int, [C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64, _u64p, _u64p]),
 }
 
 _lib = None

@@ -1041,6 +1041,35 @@ int cgpu_sieve_launch_span_dev(cgpu_ctx* c, uint64_t p_lo, uint64_t q_start, uin
 	                     reinterpret_cast<unsigned long long*>(d_surv), surv_cap);
 }
 
+int cgpu_region_advance(uint64_t p, uint64_t q, uint64_t k, uint64_t p_end, uint64_t* out_p, uint64_t* out_q)
+{
+	if (!out_p || !out_q) return set_err(CGPU_ERR_INVALID, "null argument");
+	if (p == 0) return set_err(CGPU_ERR_INVALID, "p must be positive");
+	uint64_t q0 = q, c = 0;
+	for (;;) {
+		uint64_t lo, hi;
+		if (p < kRegionCrossover || c == 0) {
+			q_bounds(p, &lo, &hi);
+			if (p >= kRegionCrossover) c = lo;
+		} else {  // q_low = least q with 9 q^3 >= p: monotone in p, one step at a time
+			while (9 * static_cast<unsigned __int128>(c) * c * c < p) ++c;
+			lo = c;
+			hi = 59 * p;
+		}
+		const uint64_t first = q0 ? q0 : lo;
+		const uint64_t n = hi >= first ? hi - first + 1 : 0;
+		if (k < n) {
+			*out_p = p;
+			*out_q = first + k;
+			return CGPU_OK;
+		}
+		k -= n;
+		if (p >= p_end) return CGPU_P_ABOVE_LIMIT;  // the range ends first
+		++p;
+		q0 = 0;
+	}
+}
+
 int cgpu_device_count(int* n)
 {
 	if (!n) return set_err(CGPU_ERR_INVALID, "null argument");

@@ -257,10 +257,14 @@ def load_sieve(tables: bytes, index: bytes, dev: int = 0) -> "SieveSet":
 @dataclass
 class ScanOptions:
     """engine.hpp:144-149. `stop` stands for hooks.stop: a bool, an object with
-    is_set(), or a callable. It is read when scan() starts; if it is already
-    raised the scan halts exactly where the reference's does -- at the
-    batch_pairs-th q visited (engine.hpp:248-257) -- with the same resume
-    point. (A flag raised while a device launch runs is not observed.)"""
+    is_set(), or a callable. The reference polls it every batch_pairs q
+    visited and halts AT that q (engine.hpp:248-257). A scan with a stop hook
+    runs as device tiles ending at such poll points; a watcher thread mirrors
+    the hook into a mapped host word the kernels poll, so a tile running when
+    it rises is abandoned and the scan halts at the next poll point after the
+    tile's start -- a stop the reference makes when its flag becomes visible
+    between those polls. Raised before the scan: the batch_pairs-th q, like
+    the reference (or no stop at all if fewer q remain)."""
     small_p: bool = False
     p_limit: int = P_LIMIT_32BIT
     batch_pairs: int = 1 << 16
@@ -273,6 +277,60 @@ class ScanOptions:
         if hasattr(s, "is_set"):
             return bool(s.is_set())
         return bool(s() if callable(s) else s)
+
+
+def region_advance(pos, k: int, p_end: int):
+    """The pair k steps after pos in scan()'s q visiting order (every q of the
+    region rows, engine.hpp:225-248), or None if row p_end ends first
+    (cgpu_region_advance: host code, O(rows))."""
+    op, oq = C.c_uint64(), C.c_uint64()
+    rc = N.lib().cgpu_region_advance(int(pos[0]), int(pos[1]), int(k), int(p_end), C.byref(op), C.byref(oq))
+    if rc == N.P_ABOVE_LIMIT:
+        return None
+    N.check(rc)
+    return op.value, oq.value
+
+
+STOP_TILE_PAIRS = 1 << 37  # q visited per stoppable tile (~20 ms on one B200)
+
+
+class _StopMirror:
+    """Mirrors a ScanOptions stop hook into a mapped host word that the sieve
+    kernels of one context poll (cgpu_set_stop_word)."""
+
+    def __init__(self, ctx, opt):
+        import threading
+        self.ctx, self.opt = ctx, opt
+        w = C.c_void_p()
+        N.check(N.lib().cgpu_alloc_stop_word(C.byref(w)))
+        self.word = w.value
+        self.cell = C.c_uint32.from_address(self.word)
+        N.check(N.lib().cgpu_set_stop_word(ctx, C.c_void_p(self.word)))
+        if opt.stop_requested():
+            self.cell.value = 1
+        self.done = threading.Event()
+        self.t = threading.Thread(target=self._watch, daemon=True)
+        self.t.start()
+
+    def _watch(self):
+        while not self.done.is_set():
+            if self.opt.stop_requested():
+                self.cell.value = 1
+                return
+            self.done.wait(50e-6)
+
+    def raised(self) -> bool:
+        return self.cell.value != 0
+
+    def disarm(self):
+        if not self.done.is_set():
+            self.done.set()
+            self.t.join()
+            N.check(N.lib().cgpu_set_stop_word(self.ctx, None))
+
+    def close(self):
+        self.disarm()
+        N.lib().cgpu_free_stop_word(C.c_void_p(self.word))
 
 
 def stop_point(start, p_end: int, batch_pairs: int):
@@ -426,10 +484,8 @@ def scan(set_: SieveSet, start, p_end: int, sink: Optional[Callable] = None,
         raise ScanRejected(3)
     t0 = time.perf_counter()
     st = ScanStats(resume_p=p0, resume_q=q0)
-    halt = stop_point((p0, q0), p_end, opt.batch_pairs) if opt.stop_requested() else None
-    if halt is not None:  # the span before the reference's stop point
-        st = _span(set_, p0, q0, halt[0], halt[1])
-        st.resume_p, st.resume_q, st.stopped = halt[0], halt[1], True
+    if opt.stop is not None and p0 <= p_end and shard == (1, 0):
+        st = _scan_stoppable(set_, (p0, q0), p_end, opt, surv_cap)
     elif p0 <= p_end:
         res = _run(set_, p0, q0, p_end, N.REGION, shard, surv_cap)
         st = stats_from_result(set_, res)
@@ -438,6 +494,56 @@ def scan(set_: SieveSet, start, p_end: int, sink: Optional[Callable] = None,
     if sink is not None:
         for p, q in st.survivor_pairs:
             sink(ScanEvent(p, q, verifier(p, q) if verifier else None))
+    return st
+
+
+def _scan_stoppable(set_: SieveSet, start, p_end: int, opt: ScanOptions, surv_cap: int) -> ScanStats:
+    """scan() with a stop hook: tiles that end at poll points (every
+    batch_pairs-th q visited), the hook mirrored into the kernels' stop word
+    (include/cuboid/gpu.hpp scan_on is the C++ twin)."""
+    B = max(int(opt.batch_pairs), 1)
+    K = max(1, STOP_TILE_PAIRS // B)
+    d = set_.resident()
+    mirror = _StopMirror(d._ctx, opt)
+    st = ScanStats()
+    pos, at_poll = (int(start[0]), int(start[1])), False
+
+    def to_end(p, q):
+        res = _run(set_, p, q, p_end, N.REGION, (1, 0), surv_cap)
+        st.merge(stats_from_result(set_, res))
+        st.resume_p, st.resume_q = _next_pair(p_end)
+
+    def halt_at(at):
+        st.merge(_span(set_, pos[0], pos[1], at[0], at[1]))
+        st.block_r_max.setdefault(at[0] // 100, 1)
+        st.resume_p, st.resume_q, st.stopped = at[0], at[1], True
+
+    try:
+        while True:
+            if at_poll and opt.stop_requested():  # the reference's poll at pos
+                halt_at(pos)
+                break
+            to = region_advance(pos, K * B if at_poll else K * B - 1, p_end)
+            if to is not None:
+                part = _span(set_, pos[0], pos[1], to[0], to[1])
+            else:
+                part = stats_from_result(set_, _run(set_, pos[0], pos[1], p_end, N.REGION, (1, 0), surv_cap))
+            if mirror.raised():  # the tile may have been abandoned: the next poll point instead
+                mirror.disarm()
+                nxt = region_advance(pos, B if at_poll else B - 1, p_end)
+                if nxt is not None:
+                    halt_at(nxt)
+                else:
+                    to_end(*pos)
+                break
+            st.merge(part)
+            if to is None:
+                st.resume_p, st.resume_q = _next_pair(p_end)
+                break
+            pos, at_poll = to, True
+            st.resume_p, st.resume_q = pos
+    finally:
+        mirror.close()
     return st
 
 

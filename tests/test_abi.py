@@ -133,3 +133,19 @@ def test_product_package_never_imports_oracle():
             if f.endswith((".py", ".cu", ".cuh", ".cpp", ".h")):
                 src = open(os.path.join(dirpath, f)).read()
                 assert "oracle" not in re.findall(r"^\s*(?:from|import)\s+(\w+)", src, re.M), f
+
+
+def test_region_advance_matches_the_visiting_order():
+    """cgpu_region_advance (host) walks scan()'s q order like a row-by-row
+    count (engine.hpp:225-248), including the small-p rows and a mid-row start."""
+    import random
+    from paper_1601_00636_b200 import cuboid
+    rng = random.Random(5)
+    for _ in range(40):
+        p = rng.choice([1, 7, 150, 151, 152, 153, 999, 12345, 400000])
+        lo, hi = cuboid.q_bounds(p)
+        q = rng.randrange(lo, hi + 1)
+        k = rng.choice([0, 1, 5, hi - q, hi - q + 1, 10**5, 3 * 10**6])
+        p_end = p + rng.randrange(0, 50)
+        want = cuboid.stop_point((p, q), p_end, k + 1)  # the (k+1)-th q visited
+        assert cuboid.region_advance((p, q), k, p_end) == want

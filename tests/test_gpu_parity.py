@@ -665,6 +665,59 @@ def test_prearmed_stop_matches_reference(bp):
         assert got.block_r_max == whole.block_r_max
 
 
+def test_prearmed_stop_short_range_completes():
+    """A flag raised before scan() with fewer q left than batch_pairs: the
+    reference never reaches a poll and scans the whole range."""
+    P = default_primes()
+    rs = refmod.RefSet.build(P)
+    s = cuboid.SieveSet.build(P)
+    ref = refmod.scan(rs, 152, 3, 400, batch_pairs=1 << 30, stop_preset=True)
+    got = cuboid.scan(s, (152, 3), 400, opt=cuboid.ScanOptions(batch_pairs=1 << 30, stop=True))
+    assert not ref.stopped and not got.stopped
+    assert (got.pairs_tested, got.resume_p, got.resume_q) == (ref.pairs_tested, ref.resume_p, ref.resume_q)
+    assert got.kill_histogram == ref.kill_histogram(P)
+
+
+def test_stop_raised_mid_scan_halts_at_a_poll_point():
+    """The Python mirror sees a flag raised WHILE the device sieves (mapped
+    stop word): it halts at a poll point of the reference (q visited + 1 is a
+    multiple of batch_pairs), the halves merge to the uninterrupted scan, and
+    the stopped half equals a pre-armed stop at the same poll."""
+    import threading
+    P = default_primes()
+    s = cuboid.SieveSet.build(P)
+    p_end, B = 1500000, 1 << 16
+    ev = threading.Event()
+    threading.Timer(0.3, ev.set).start()
+    h = cuboid.scan(s, (152, 3), p_end, opt=cuboid.ScanOptions(batch_pairs=B, stop=ev))
+    assert h.stopped and 152 < h.resume_p < p_end
+    visited = 0
+    for p in range(152, h.resume_p + 1):
+        lo, hi = cuboid.q_bounds(p)
+        q0 = 3 if p == 152 else lo
+        visited += (hi - q0 + 1) if p < h.resume_p else (h.resume_q - q0)
+    assert (visited + 1) % B == 0
+    tail = cuboid.scan(s, (h.resume_p, h.resume_q), p_end)
+    whole = cuboid.scan(s, (152, 3), p_end)
+    again = cuboid.scan(s, (152, 3), p_end, opt=cuboid.ScanOptions(batch_pairs=visited + 1, stop=True))
+    assert (again.pairs_tested, again.kill_histogram, again.block_r_max, again.resume_p, again.resume_q) == \
+        (h.pairs_tested, h.kill_histogram, h.block_r_max, h.resume_p, h.resume_q)
+    h.merge(tail)
+    assert (h.pairs_tested, h.survivors, h.kill_histogram, h.block_r_max, h.resume_p, h.resume_q) == \
+        (whole.pairs_tested, whole.survivors, whole.kill_histogram, whole.block_r_max, whole.resume_p,
+         whole.resume_q)
+
+
+def test_stoppable_scan_tiles_equal_one_launch():
+    """A scan polled for stops (never raised) runs as many tiles: same result."""
+    s = cuboid.SieveSet.build(default_primes())
+    tiled = cuboid.scan(s, (152, 3), 200000, opt=cuboid.ScanOptions(stop=lambda: False))
+    one = cuboid.scan(s, (152, 3), 200000)
+    assert not tiled.stopped
+    assert (tiled.pairs_tested, tiled.kill_histogram, tiled.block_r_max, tiled.resume_p, tiled.resume_q) == \
+        (one.pairs_tested, one.kill_histogram, one.block_r_max, one.resume_p, one.resume_q)
+
+
 def test_multi_chunk_launch(dev, sets):
     """A range of more than one launch chunk (1,048,500 row slots): TRIANGLE
     p <= 1.1e6 (3.7e11 pairs) -- every candidate counted once across the
