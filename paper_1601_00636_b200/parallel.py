@@ -49,35 +49,52 @@ def reduce_results(acc, brm, group=None):
     return acc, brm
 
 
-def reduce_packed(acc, brm, keys, count: int, cap: int, group=None):
+def reduce_packed(acc, brm, keys, count: int, cap: int, group=None, stored=None):
     """The whole cross-rank merge in ONE all-reduce(SUM) of a packed int64
     buffer [acc | block r_max | per-rank count | per-rank survivor slices]:
     block r_max needs no MAX because every p/100 block has exactly one owner
     (the others hold 0), and each rank's survivors land in its own zeroed
     slice, so the sum is the gather. Falls back to gather_survivors when some
-    rank has more than `cap` survivors. Returns (acc, brm, sorted (p, q))."""
+    rank has more than `cap` survivors. `stored` (default `count`) is how many
+    of this rank's `count` survivors its buffer holds: a rank whose device
+    buffer overflowed still joins every collective, and the per-rank counts
+    returned let every rank see it. Returns (acc, brm, sorted (p, q), counts)."""
     import torch
     import torch.distributed as dist
+    stored = count if stored is None else min(stored, count)
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
     na, nb = acc.numel(), brm.numel()
-    buf = torch.zeros(na + nb + world + world * cap, dtype=torch.int64, device=acc.device)
+    # [acc | brm | count per rank | stored per rank | survivor slices]
+    buf = torch.zeros(na + nb + 2 * world + world * cap, dtype=torch.int64, device=acc.device)
     buf[:na] = acc
     buf[na:na + nb] = brm.to(torch.int64)
     buf[na + nb + rank] = count
-    k = min(count, cap)
-    base = na + nb + world + rank * cap
+    buf[na + nb + world + rank] = stored
+    k = min(stored, cap)
+    base = na + nb + 2 * world + rank * cap
     buf[base:base + k] = keys[:k]
     dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=group)
     acc.copy_(buf[:na])
     brm.copy_(buf[na:na + nb].to(brm.dtype))
     counts = buf[na + nb:na + nb + world].cpu().numpy()
-    if counts.max() > cap:
-        return acc, brm, gather_survivors(keys, count, group)
-    surv = buf[na + nb + world:].view(world, cap).cpu().numpy()
-    allk = np.concatenate([surv[r][:counts[r]] for r in range(world)]).astype(np.uint64)
+    held = buf[na + nb + world:na + nb + 2 * world].cpu().numpy()
+    if held.max() > cap:
+        return acc, brm, gather_survivors(keys, stored, group), counts
+    surv = buf[na + nb + 2 * world:].view(world, cap).cpu().numpy()
+    allk = np.concatenate([surv[r][:held[r]] for r in range(world)]).astype(np.uint64)
     allk.sort()
-    return acc, brm, np.stack([allk >> np.uint64(32), allk & np.uint64(0xFFFFFFFF)], 1)
+    return acc, brm, np.stack([allk >> np.uint64(32), allk & np.uint64(0xFFFFFFFF)], 1), counts
+
+
+def check_survivor_capacity(counts, surv_cap: int):
+    """After the collectives: raise on EVERY rank if any rank's survivors
+    exceeded its device buffer (raising before them would leave the other
+    ranks blocked in the all-reduce)."""
+    over = [r for r, c in enumerate(np.asarray(counts).tolist()) if c > surv_cap]
+    if over:
+        raise N.CudaSieveError(N.ERR_CAPACITY, f"ranks {over} have more survivors than their "
+                               f"{surv_cap}-entry buffers (counts {np.asarray(counts).tolist()})")
 
 
 def gather_survivors(keys, count: int, group=None):
@@ -206,13 +223,13 @@ class ShardedSieve:
         import torch.distributed as dist
         self.dev.synchronize()  # the context stream may differ from torch's current stream
         local_surv = int(self.acc[1].item())
-        if local_surv > self.surv_cap:
-            raise N.CudaSieveError(N.ERR_CAPACITY, f"{local_surv} survivors exceed {self.surv_cap}")
         keys = self.surv
         if dist.is_initialized() and dist.get_world_size() > 1:
-            _, _, pairs = reduce_packed(self.acc, self.brm[:max(self.nb, 1)], keys, local_surv,
-                                        cap=4096)
+            _, _, pairs, counts = reduce_packed(self.acc, self.brm[:max(self.nb, 1)], keys, local_surv,
+                                                cap=4096, stored=min(local_surv, self.surv_cap))
+            check_survivor_capacity(counts, self.surv_cap)
         else:
+            check_survivor_capacity([local_surv], self.surv_cap)
             k = np.sort(keys[:local_surv].cpu().numpy().astype(np.uint64))
             pairs = np.stack([k >> np.uint64(32), k & np.uint64(0xFFFFFFFF)], 1)
         a = self.acc.cpu().numpy()

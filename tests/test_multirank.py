@@ -130,7 +130,8 @@ def _worker(rank, world, port_, case, out):
     parallel.reduce_results(acc_t, brm_t)
     surv = parallel.gather_survivors(keys_t, len(keys))
     # the single-collective form, with a cap small enough to hit the fallback too
-    _, _, surv2 = parallel.reduce_packed(acc2, brm2, keys_t, len(keys), cap=64)
+    _, _, surv2, counts = parallel.reduce_packed(acc2, brm2, keys_t, len(keys), cap=64)
+    assert int(sum(counts)) == int(acc_t[1])
     assert acc2.tolist() == acc_t.tolist() and brm2.tolist() == brm_t.tolist()
     assert surv2.tolist() == surv.tolist()
     out[rank] = (acc_t.numpy().tolist(), brm_t.numpy().tolist(), surv.tolist())
@@ -163,3 +164,34 @@ def test_gloo_reduction_equals_single_process(world, case):
         assert acc[2:] == full["hist"].astype(np.int64).tolist()
         assert {lo // 100 + i: v for i, v in enumerate(brm)} == want_brm
         assert surv == full["survivor_pairs"].tolist()
+
+
+def _overflow_worker(rank, world, port_, out):
+    """Rank 1's device buffer held only 3 of its 10 survivors: both ranks
+    finish the collectives and both raise (raising before the
+    all-reduce left the other ranks blocked in it)."""
+    from paper_1601_00636_b200 import _native as N
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port_)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    acc = torch.zeros(4, dtype=torch.int64)
+    brm = torch.zeros(2, dtype=torch.int32)
+    count = 10 if rank == 1 else 2
+    acc[1] = count
+    keys = torch.arange(1, 4, dtype=torch.int64) + (1000 << 32) * (rank + 1)
+    _, _, pairs, counts = parallel.reduce_packed(acc, brm, keys, count, cap=64, stored=min(count, 3))
+    try:
+        parallel.check_survivor_capacity(counts, 3)
+        out[rank] = "no error"
+    except N.CudaSieveError as e:
+        out[rank] = ("raised", e.code, counts.tolist(), len(pairs))
+    dist.destroy_process_group()
+
+
+def test_survivor_overflow_raises_on_every_rank():
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_overflow_worker, args=(2, _free_port(), out), nprocs=2, join=True)
+    from paper_1601_00636_b200 import _native as N
+    for r in range(2):
+        assert out[r] == ("raised", N.ERR_CAPACITY, [2, 10], 5)  # the 2 + 3 survivors held
