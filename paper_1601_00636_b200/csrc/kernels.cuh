@@ -57,6 +57,10 @@ cudaError_t launch_check_padding(const PrimeJob* d_jobs, uint32_t njobs, const u
 constexpr uint32_t kCubeThreads = 256;
 constexpr int kCubePairs = 4;  // (a,b) pairs per thread in k_cube
 constexpr int kCubeF2Pairs = 16;  // (a,b) pairs per thread in k_cube_f2 (two per FFMA2)
+#ifndef CGPU_CUBE_SCALAR
+#define CGPU_CUBE_SCALAR 0
+#endif
+constexpr int kCubeF2Scalar = CGPU_CUBE_SCALAR;  // of them evaluated with scalar FFMA (fmalite or fmaheavy)
 constexpr uint32_t kCubeF2MaxR = 2039;  // largest prime with h + 4h^2 < 2^22, h = (r-1)/2
 constexpr uint32_t kPermThreads = 256;
 constexpr uint32_t kRow1Threads = 128;

@@ -224,10 +224,28 @@ __global__ void __launch_bounds__(kCubeThreads) k_cube_f2(const PrimeJob* __rest
 	__syncthreads();
 	const uint32_t tbytes = (rr + 7) >> 3;
 	const uint32_t lane = threadIdx.x & 31;
-	constexpr int NP = PAIRS / 2;  // FFMA2 pair slots
+	constexpr int SC = kCubeF2Scalar;      // pairs on scalar FFMA (either FMA pipe)
+	constexpr int NP = (PAIRS - SC) / 2;  // FFMA2 pair slots (heavy pipe)
 	for (uint32_t base = blockIdx.x * per_cta; base < rr; base += gridDim.x * per_cta) {
-		unsigned long long C1[NP], C2[NP], C3[NP], C4[NP], V0[NP];
+		unsigned long long C1[NP > 0 ? NP : 1], C2[NP > 0 ? NP : 1], C3[NP > 0 ? NP : 1], C4[NP > 0 ? NP : 1],
+		    V0[NP > 0 ? NP : 1];
+		float S1[SC > 0 ? SC : 1], S2[SC > 0 ? SC : 1], S3[SC > 0 ? SC : 1], S4[SC > 0 ? SC : 1],
+		    W0[SC > 0 ? SC : 1];
 		uint32_t mn[PAIRS];
+#pragma unroll
+		for (int k = 0; k < SC; ++k) {
+			const uint32_t i = base + (2 * NP + k) * kCubeThreads + threadIdx.x;
+			uint32_t a = __umulhi(i, m), b = i - a * r;
+			if (b >= r) { b -= r; ++a; }
+			uint32_t cu[5];
+			mod_coeffs(i < rr ? a : 0, i < rr ? b : 0, r, m, cu);
+			S4[k] = balanced(cu[0], r);
+			S3[k] = balanced(cu[1], r);
+			S2[k] = balanced(cu[2], r);
+			S1[k] = balanced(cu[3], r);
+			W0[k] = 12582912.0f + balanced(cu[4], r);
+			mn[2 * NP + k] = 0xffffffffu;
+		}
 #pragma unroll
 		for (int j = 0; j < NP; ++j) {
 			float c[2][5];
@@ -267,6 +285,14 @@ __global__ void __launch_bounds__(kCubeThreads) k_cube_f2(const PrimeJob* __rest
 			for (int j = 0; j < NP; ++j) {
 				mn[2 * j] = min(mn[2 * j], static_cast<uint32_t>(v[j]) * rinv + w);
 				mn[2 * j + 1] = min(mn[2 * j + 1], static_cast<uint32_t>(v[j] >> 32) * rinv + w);
+			}
+#pragma unroll
+			for (int k = 0; k < SC; ++k) {
+				float x = fmaf(S4[k], bp.w, W0[k]);
+				x = fmaf(S3[k], bp.z, x);
+				x = fmaf(S2[k], bp.y, x);
+				x = fmaf(S1[k], bp.x, x);
+				mn[2 * NP + k] = min(mn[2 * NP + k], __float_as_uint(x) * rinv + w);
 			}
 		}
 #pragma unroll
