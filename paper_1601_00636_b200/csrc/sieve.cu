@@ -676,7 +676,11 @@ __global__ void __launch_bounds__(kSieveThreads, kSieveMinBlocks) k_sieve(const 
 	const uint32_t n_chunks = plan_chunks(a.n_slots);
 	const unsigned long long W = a.chunk_off[n_chunks];
 	const unsigned long long nwarps = static_cast<unsigned long long>(gridDim.x) * kSieveWarps;
+#ifdef CGPU_REVERSE_SLICES  // experiment: CTA b takes the slices of CTA grid-1-b (per-SM speed vs work)
+	const unsigned long long gw = static_cast<unsigned long long>(gridDim.x - 1 - blockIdx.x) * kSieveWarps + wib;
+#else
 	const unsigned long long gw = static_cast<unsigned long long>(blockIdx.x) * kSieveWarps + wib;
+#endif
 	unsigned long long ws = W * gw / nwarps;  // W < 2^40, nwarps < 2^20
 	const unsigned long long we = W * (gw + 1) / nwarps;
 

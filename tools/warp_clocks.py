@@ -32,6 +32,9 @@ for spec in sys.argv[1].split(","):  # NAME or NAME/G/g (block-cyclic shard g of
           f"end min/p10/p50/p90/max {np.percentile(en, [0, 10, 50, 90, 100]).round(1).tolist()}; "
           f"busy mean {busy.mean():.1f} std {busy.std():.1f}")
     sm_end = np.array([en[sm == s].max() for s in np.unique(sm)])
+    if os.environ.get("WCLK_DUMP"):  # per-SM last-warp end and busy sum, for offline analysis
+        np.save(os.path.join(os.environ["WCLK_DUMP"], spec.replace("/", "_") + ".npy"),
+                np.stack([np.arange(len(a)), st, en, sm], 1))  # warp index (blockIdx * warps + w), start, end, smid
     print(f"   per-SM last warp end: min {sm_end.min():.1f} mean {sm_end.mean():.1f} max {sm_end.max():.1f}")
     order = np.argsort(-en)[:8]
     print("   latest warps (idx, end us, sm):", [(int(i), round(float(en[i]), 1), int(sm[i])) for i in order])
