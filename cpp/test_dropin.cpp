@@ -331,6 +331,43 @@ int main()
 		std::printf("multi-GPU clique of %zu device(s) checked\n", devs.size());
 	}
 
+	// verify_pair and verify_small_region (engine.hpp:66-95, 609-640) with the
+	// sieve part on the device: the reference's verdicts and counts
+	{
+		for (SearchPair pr : {SearchPair{152, 3}, SearchPair{153, 7000}, SearchPair{2, 1}, SearchPair{7, 4}}) {
+			const PairVerdict g = gpu::verify_pair(ref_default, pr, false);
+			const PairVerdict r = verify_pair(&ref_default, pr, false);
+			CHECK(g.kind == r.kind && g.prime == r.prime && g.t == r.t);
+		}
+		CHECK(gpu::verify_pair(ref_default, {152, 3}, false).prime == 11);  // test_engine.cpp:51-59
+		int bad = 0;
+		try { gpu::verify_pair(ref_default, {5, 5}, false); } catch (const std::invalid_argument&) { ++bad; }
+		try { gpu::verify_pair(ref_default, {6, 4}, false); } catch (const std::invalid_argument&) { ++bad; }
+		try { gpu::verify_pair(SieveSet{}, {7, 4}, false); } catch (const std::invalid_argument&) { ++bad; }
+		CHECK(bad == 3);
+		std::vector<SearchPair> many;
+		for (uint64_t p = 2; p < 400; ++p)
+			for (uint64_t q = 1; q < p; q += 7)
+				if (std::gcd(p, q) == 1) many.push_back({p, q});
+		const std::vector<int32_t> ranks = gpu::classify(ref_default, many);
+		bool ranks_same = true;
+		for (size_t i = 0; i < many.size(); ++i) {
+			int32_t want = -1;
+			for (size_t k = 0; k < ref_default.prime_count() && want < 0; ++k)
+				if (ref_default.is_unsolvable(k, many[i].p, many[i].q)) want = static_cast<int32_t>(k);
+			ranks_same &= ranks[i] == want;
+		}
+		CHECK(ranks_same);
+		for (const SieveSet* s : {&ref_default, &weak}) {
+			const SmallRegionSummary g = gpu::verify_small_region(*s);
+			const SmallRegionSummary r = verify_small_region(*s);
+			CHECK(g.pairs == r.pairs && g.sieved_out == r.sieved_out && g.survivors == r.survivors &&
+			      g.no_integer_root == r.no_integer_root && g.root_fails == r.root_fails &&
+			      g.candidates == r.candidates);
+		}
+		CHECK(gpu::verify_small_region(ref_default).pairs == 413362);  // test_engine.cpp:416-423
+	}
+
 	// TRIANGLE (BASELINE config 1: 32 odd primes, 2 <= p <= 2000)
 	const std::vector<uint32_t> P32 = odd_primes(32);
 	const SieveSet s32 = SieveSet::build(P32);

@@ -10,6 +10,10 @@
 //                     sink, opt)
 //   cuboid::gpu::scan_triangle(set, lo, hi, sink)   the TRIANGLE loop of the BASELINE configs
 //                                          (verify_small_region's pattern over q < p, engine.hpp:613-625)
+//   cuboid::gpu::verify_pair(set, pr, bypass)   replaces verify_pair        engine.hpp:66-95
+//   cuboid::gpu::verify_small_region(set)  replaces verify_small_region     engine.hpp:609-640
+//   cuboid::gpu::classify(set, pairs)      is_unsolvable in rank order      sievetable.hpp:199-205
+//   cuboid::gpu::SearchController          replaces SearchController        engine.hpp:429-595
 //
 // Same argument meaning, return types and exceptions as the reference:
 // std::invalid_argument / std::overflow_error from the builders, ScanRejected{code}
@@ -46,6 +50,7 @@
 #include <functional>
 #include <map>
 #include <mutex>
+#include <numeric>
 #include <optional>
 #include <stdexcept>
 #include <string>
@@ -109,7 +114,8 @@ private:
 };
 
 // One device context per process and device (one process per GPU), holding
-// the resident table set.
+// the resident table set. Its lock is recursive: a scan sink may call
+// gpu::verify_pair / classify on the same device.
 class Context {
 public:
 	explicit Context(int device = 0) : device_(device) { check(cgpu_create(device, nullptr, &ctx_), "cgpu_create"); }
@@ -152,13 +158,13 @@ public:
 		return n;
 	}
 
-	std::mutex& mutex() { return mu_; }
+	std::recursive_mutex& mutex() { return mu_; }
 
 private:
 	int device_;
 	cgpu_ctx* ctx_ = nullptr;
 	Residency res_;
-	std::mutex mu_;
+	std::recursive_mutex mu_;
 };
 
 // Several GPUs driven from this one process (cgpu_multi: one context per
@@ -215,13 +221,13 @@ public:
 		return n;
 	}
 
-	std::mutex& mutex() { return mu_; }
+	std::recursive_mutex& mutex() { return mu_; }
 
 private:
 	std::vector<int> devices_;
 	cgpu_multi* m_ = nullptr;
 	Residency res_;
-	std::mutex mu_;
+	std::recursive_mutex mu_;
 };
 
 inline Context& context(int device = 0)
@@ -250,7 +256,7 @@ inline SieveSet build_set(const std::vector<uint32_t>& primes, int device = 0,
                           int algorithm = CGPU_BUILD_PRODUCTION)
 {
 	Context& c = context(device);
-	std::lock_guard<std::mutex> lk(c.mutex());
+	std::lock_guard<std::recursive_mutex> lk(c.mutex());
 	const uint32_t n = static_cast<uint32_t>(primes.size());
 	std::vector<uint32_t> offsets(n);
 	uint64_t total = 0;
@@ -469,7 +475,7 @@ ScanStats scan_on(Ctx& c, const SieveSet& set, SearchPair start, uint64_t p_end,
 	st.resume_p = start.p;
 	st.resume_q = start.q;
 	const auto t0 = std::chrono::steady_clock::now();
-	std::lock_guard<std::mutex> lk(c.mutex());
+	std::lock_guard<std::recursive_mutex> lk(c.mutex());
 	c.ensure_resident(set);
 	auto publish = [&](uint64_t p, uint64_t q) {  // flush_hooks (engine.hpp:218-223)
 		if (opt.hooks.current_p) opt.hooks.current_p->store(p, std::memory_order_relaxed);
@@ -583,7 +589,7 @@ inline ScanStats scan_triangle(const SieveSet& set, uint64_t p_lo, uint64_t p_hi
 	const auto t0 = std::chrono::steady_clock::now();
 	if (p_lo <= p_hi) {
 		auto go = [&](auto& c) {
-			std::lock_guard<std::mutex> lk(c.mutex());
+			std::lock_guard<std::recursive_mutex> lk(c.mutex());
 			c.ensure_resident(set);
 			detail::fold(set, detail::run(c, set, p_lo, 0, p_hi, CGPU_TRIANGLE), st, sink);
 		};
@@ -595,6 +601,72 @@ inline ScanStats scan_triangle(const SieveSet& set, uint64_t p_lo, uint64_t p_hi
 	}
 	st.elapsed = std::chrono::steady_clock::now() - t0;
 	return st;
+}
+
+// ---- the final check and the small region ---------------------------------------
+
+// First-killer ranks of explicit pairs (the sieve part of verify_pair,
+// engine.hpp:72-78; SieveSet::is_unsolvable in rank order on the device,
+// cgpu_classify): -1 where no table rejects the pair.
+inline std::vector<int32_t> classify(const SieveSet& set, const std::vector<SearchPair>& pairs, int device = 0)
+{
+	std::vector<int32_t> ranks(pairs.size(), -1);
+	if (pairs.empty()) return ranks;
+	Context& c = context(device);
+	std::lock_guard<std::recursive_mutex> lk(c.mutex());
+	c.ensure_resident(set);
+	std::vector<uint64_t> pq(2 * pairs.size());
+	for (size_t i = 0; i < pairs.size(); ++i) {
+		pq[2 * i] = pairs[i].p;
+		pq[2 * i + 1] = pairs[i].q;
+	}
+	check(cgpu_classify(c.get(), pq.data(), pairs.size(), ranks.data()), "classify");
+	return ranks;
+}
+
+// verify_pair (engine.hpp:66-95): the same validation and verdicts; without
+// bypass the sieve part runs on the device, the exact part (GMP quintic roots,
+// perfect squares, inequalities) is the reference's own code.
+inline PairVerdict verify_pair(const SieveSet& set, const SearchPair& pr, bool bypass_sieve, int device = 0)
+{
+	if (pr.p == 0 || pr.q == 0 || pr.p == pr.q)
+		throw std::invalid_argument("verify_pair: requires positive p != q");
+	if (std::gcd(pr.p, pr.q) != 1) throw std::invalid_argument("verify_pair: requires gcd(p,q) = 1");
+	if (!bypass_sieve) {
+		if (set.empty()) throw std::invalid_argument("verify_pair: sieve tables not loaded");
+		const int32_t rank = classify(set, {pr}, device)[0];
+		if (rank >= 0) return PairVerdict::sieved_out(set.prime_at(static_cast<size_t>(rank)));
+	}
+	return cuboid::verify_pair(&set, pr, /*bypass_sieve=*/true);
+}
+
+// verify_small_region (engine.hpp:609-640): every coprime p != q pair of the
+// region rows p <= 151 sieved on the device (scan with small_p), each
+// survivor through the reference's exact check; a candidate throws, as there.
+inline SmallRegionSummary verify_small_region(const SieveSet& set, int device = 0)
+{
+	if (set.empty()) throw std::invalid_argument("verify_small_region: empty sieve set");
+	SmallRegionSummary sum;
+	ScanOptions opt;
+	opt.small_p = true;
+	const ScanStats st = scan(
+	    set, {1, 1}, 151,
+	    [&](const ScanEvent& e) {
+		    switch (e.verdict.kind) {
+		    case PairVerdict::Kind::NoIntegerRoot: ++sum.no_integer_root; break;
+		    case PairVerdict::Kind::RootFailsInequalities: ++sum.root_fails; break;
+		    case PairVerdict::Kind::CuboidCandidate:
+			    ++sum.candidates;
+			    throw std::runtime_error("cuboid candidate found at p=" + std::to_string(e.p) +
+			                             ", q=" + std::to_string(e.q) + ", t=" + e.verdict.t.get_str());
+		    default: break;
+		    }
+	    },
+	    opt, device);
+	sum.pairs = st.pairs_tested;
+	sum.survivors = st.survivors;
+	sum.sieved_out = st.pairs_tested - st.survivors;
+	return sum;
 }
 
 // ---- the search controller (engine.hpp:429-595) on the GPU ----------------------
