@@ -524,7 +524,7 @@ int begin_set(cgpu_ctx* c, const uint32_t* primes, uint32_t n)
 	c->primes.assign(primes, primes + n);
 	c->offsets = offs;
 	c->total_bytes = total;
-	CK(c->packed.ensure(total + 8));  // k_derive reads aligned words one past the last byte
+	CK(c->packed.ensure(total + 64));  // k_derive stages 16-byte aligned spans one word past the last byte
 	return CGPU_OK;
 }
 

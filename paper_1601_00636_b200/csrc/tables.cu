@@ -372,17 +372,19 @@ __global__ void __launch_bounds__(kPermThreads) k_permute(const PrimeJob* __rest
 // Packed reference tables -> row-extended words (common.cuh ext_row_words):
 // word j of row a holds bits u(a, (32j + l) mod r), l = 0..31. One CTA per
 // work item {job, first row, rows} (built on the host, <= kDeriveItemWords
-// output words each): the CTA stages the item's packed bits in shared memory
-// with coalesced word loads, then each thread builds output words from it
-// (one or two funnel shifts across the row wrap) and stores them coalesced;
-// killable[k] bit 0 is set when any word written for table k is nonzero, bit
-// 1 when the loaded row 0 holds a set bit. Row 0 is written as zeros unless
-// keep_row0: scan() skips primes with p mod r = 0 (engine.hpp:240-242), while
-// the TRIANGLE loop's is_unsolvable reads the row like any other
-// (sievetable.hpp:199-205, engine.hpp:619-623); canonical tables have a zero
-// row 0 anyway, so the two layouts differ only for non-canonical loaded bytes.
-// (Per-word gathers straight from L2 were latency-bound: 113-145 us for the
-// 256-prime set.)
+// output words each): one thread stages the item's packed bytes in shared
+// memory with a single TMA bulk copy (cp.async.bulk, completion on an
+// mbarrier; the item's bits are one contiguous byte range), then each thread
+// builds output words from it (one or two funnel shifts across the row wrap)
+// and stores them coalesced; killable[k] bit 0 is set when any word written
+// for table k is nonzero, bit 1 when the loaded row 0 holds a set bit. Row 0
+// is written as zeros unless keep_row0: scan() skips primes with p mod r = 0
+// (engine.hpp:240-242), while the TRIANGLE loop's is_unsolvable reads the row
+// like any other (sievetable.hpp:199-205, engine.hpp:619-623); canonical
+// tables have a zero row 0 anyway, so the two layouts differ only for
+// non-canonical loaded bytes. (Per-word gathers straight from L2 were
+// latency-bound: 113-145 us for the 256-prime set; a thread-strided staging
+// loop of word loads 29.9 us, 31% of it waiting on those loads.)
 __global__ void __launch_bounds__(kDeriveThreads) k_derive(const PrimeJob* __restrict__ jobs,
                                                            const uint4* __restrict__ items,
                                                            const uint8_t* __restrict__ packed,
@@ -390,19 +392,38 @@ __global__ void __launch_bounds__(kDeriveThreads) k_derive(const PrimeJob* __res
                                                            uint32_t* __restrict__ killable,
                                                            int keep_row0)
 {
-	extern __shared__ uint32_t s_bits[];
+	extern __shared__ uint4 s_raw[];  // 16-byte aligned staging of the item's bytes
+	__shared__ __align__(8) unsigned long long s_mbar;
+	const uint32_t* s_bits = reinterpret_cast<const uint32_t*>(s_raw);
 	const uint4 it = items[blockIdx.x];  // {job, first row, rows, -}
 	const PrimeJob job = jobs[it.x];
-	const uint32_t r = job.r, m = job.m, S = ext_row_words(r);
-	// global bit range of the rows, staged from its first aligned word
+	const uint32_t r = job.r, S = ext_row_words(r);
+	// global bit range of the rows, staged from its 16-byte aligned first byte
 	const uint64_t bit0 = 8ull * job.byte_off + static_cast<uint64_t>(it.y) * r;
-	const uint64_t w0 = bit0 >> 5;
 	const uint32_t nbits = it.z * r;
-	const uint32_t nw = static_cast<uint32_t>((((bit0 & 31) + nbits + 31) >> 5) + 1);
-	const uint32_t* words32 = reinterpret_cast<const uint32_t*>(packed);
-	for (uint32_t i = threadIdx.x; i < nw; i += blockDim.x) s_bits[i] = __ldg(words32 + w0 + i);
+	const uint64_t byte_lo = (bit0 >> 3) & ~15ull;
+	const uint64_t byte_hi = (((bit0 + nbits + 7) >> 3) + 8 + 15) & ~15ull;  // + a word past the end
+	const uint32_t nbytes = static_cast<uint32_t>(byte_hi - byte_lo);
+	const uint32_t mbar = static_cast<uint32_t>(__cvta_generic_to_shared(&s_mbar));
+	if (threadIdx.x == 0) {
+		asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mbar));
+		asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+		asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mbar), "r"(nbytes) : "memory");
+		asm volatile(
+		    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+		        static_cast<uint32_t>(__cvta_generic_to_shared(s_raw))),
+		    "l"(packed + byte_lo), "r"(nbytes), "r"(mbar)
+		    : "memory");
+	}
+	if (threadIdx.x == 0)  // one waiter; the others sleep in the barrier instead of spinning
+		asm volatile(
+		    "{\n\t.reg .pred done;\n"
+		    "WAIT_%=:\n\t"
+		    "mbarrier.try_wait.parity.shared::cta.b64 done, [%0], 0;\n\t"
+		    "@!done bra WAIT_%=;\n}" ::"r"(mbar)
+		    : "memory");
 	__syncthreads();
-	const uint32_t sh = static_cast<uint32_t>(bit0 & 31);  // bit offset of row it.y in s_bits
+	const uint32_t sh = static_cast<uint32_t>(bit0 - 8 * byte_lo);  // bit offset of row it.y in s_bits
 	// 32 bits starting at local bit i of the staged rows
 	auto bits32 = [&](uint32_t i) {
 		const uint32_t li = i + sh;
@@ -411,31 +432,71 @@ __global__ void __launch_bounds__(kDeriveThreads) k_derive(const PrimeJob* __res
 	bool any = false, row0_set = false;
 	const uint32_t words = it.z * S;
 	const uint32_t mS = barrett_m(S);
-	for (uint32_t w = threadIdx.x; w < words; w += blockDim.x) {
-		uint32_t a = __umulhi(w, mS), j = w - a * S;  // local row, word in row
-		if (j >= S) { j -= S; ++a; }
-		uint32_t b = mod_full(32 * j, r, m);  // offset of bit 0 of the word in the row
-		const uint32_t row0 = a * r;
-		uint32_t word;
-		if (r >= 32) {  // at most one wrap: bits [b, r) then [0, 32 - (r - b))
-			const uint32_t head = r - b;
-			word = bits32(row0 + b);
-			if (head < 32) word = (word & ((1u << head) - 1)) | (bits32(row0) << head);
-		} else {  // small r: the row repeats inside one word
-			const uint32_t row = bits32(row0) & ((1u << r) - 1);
-			word = 0;
+	const uint32_t m = job.m;
+	const uint64_t E0 = job.ext_base + static_cast<uint64_t>(it.y) * S;  // first output word
+	if (r >= 32) {
+		// Each thread writes one 16-byte aligned group of 4 output words (one
+		// vector store; partial groups at the item's ends store word by word):
+		// the row/word split is computed once per group and stepped after.
+		const uint64_t g0 = E0 & ~3ull;
+		const uint32_t ngroups = static_cast<uint32_t>((E0 + words - g0 + 3) >> 2);
+		for (uint32_t gi = threadIdx.x; gi < ngroups; gi += blockDim.x) {
+			const uint64_t A = g0 + 4ull * gi;
+			const int64_t w0 = static_cast<int64_t>(A) - static_cast<int64_t>(E0);  // local word of slot 0
+			const uint32_t wf = w0 < 0 ? 0u : static_cast<uint32_t>(w0);
+			uint32_t a = __umulhi(wf, mS), j = wf - a * S;  // local row, word in row
+			if (j >= S) { j -= S; ++a; }
+			uint32_t v[4];
+			bool in[4];
+#pragma unroll
+			for (int q = 0; q < 4; ++q) {
+				const int64_t wl = w0 + q;
+				in[q] = wl >= 0 && wl < static_cast<int64_t>(words);
+				v[q] = 0;
+				if (!in[q]) continue;
+				uint32_t b = 32 * j;  // 32 j < r + 32 <= 2 r: one conditional subtraction
+				if (b >= r) b -= r;
+				const uint32_t row0 = a * r, head = r - b;  // at most one wrap: [b, r) then [0, 32 - head)
+				uint32_t word = bits32(row0 + b);
+				if (head < 32) word = (word & ((1u << head) - 1)) | (bits32(row0) << head);
+				if (it.y + a == 0) {  // row p = 0 mod r: scan() never probes it (engine.hpp:240-242)
+					row0_set |= word != 0;
+					if (!keep_row0) word = 0;
+				}
+				v[q] = word;
+				any |= word != 0;
+				if (++j == S) {
+					j = 0;
+					++a;
+				}
+			}
+			if (in[0] && in[3]) {
+				*reinterpret_cast<uint4*>(ext + A) = make_uint4(v[0], v[1], v[2], v[3]);
+			} else {
+#pragma unroll
+				for (int q = 0; q < 4; ++q)
+					if (in[q]) ext[A + q] = v[q];
+			}
+		}
+	} else {  // small r: the row repeats inside one word
+		for (uint32_t w = threadIdx.x; w < words; w += blockDim.x) {
+			uint32_t a = __umulhi(w, mS), j = w - a * S;
+			if (j >= S) { j -= S; ++a; }
+			uint32_t b = mod_full(32 * j, r, m);
+			const uint32_t row = bits32(a * r) & ((1u << r) - 1);
+			uint32_t word = 0;
 #pragma unroll 8
 			for (uint32_t l = 0; l < 32; ++l) {
 				word |= ((row >> b) & 1u) << l;
 				b = b + 1 == r ? 0 : b + 1;
 			}
+			if (it.y + a == 0) {
+				row0_set |= word != 0;
+				if (!keep_row0) word = 0;
+			}
+			ext[E0 + w] = word;
+			any |= word != 0;
 		}
-		if (it.y + a == 0) {  // row p = 0 mod r: scan() never probes it (engine.hpp:240-242)
-			row0_set |= word != 0;
-			if (!keep_row0) word = 0;
-		}
-		ext[job.ext_base + static_cast<uint64_t>(it.y) * S + w] = word;
-		any |= word != 0;
 	}
 	const bool any_cta = __syncthreads_or(any);
 	const bool row0_cta = __syncthreads_or(row0_set);
@@ -571,8 +632,9 @@ cudaError_t launch_derive(const PrimeJob* d_jobs, const uint4* d_items, uint32_t
                           uint32_t* d_ext, uint32_t* d_killable, int keep_row0, cudaStream_t s)
 {
 	if (!nitems) return cudaSuccess;
-	// staged bits: <= kDeriveItemWords output words cover <= kDeriveItemWords * 32 bits... plus slack
-	const size_t smem = sizeof(uint32_t) * (kDeriveItemWords + 4);
+	// staged bytes: <= kDeriveItemWords output words cover <= kDeriveItemWords * 32 bits, plus the
+	// 16-byte alignment of both ends and a word past the last byte
+	const size_t smem = sizeof(uint32_t) * kDeriveItemWords + 48;
 	k_derive<<<nitems, kDeriveThreads, smem, s>>>(d_jobs, d_items, d_packed, d_ext, d_killable, keep_row0);
 	return cudaGetLastError();
 }
