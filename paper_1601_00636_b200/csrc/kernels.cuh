@@ -64,7 +64,11 @@ constexpr int kCubeF2Scalar = CGPU_CUBE_SCALAR;  // of them evaluated with scala
 constexpr uint32_t kCubeF2MaxR = 2039;  // largest prime with h + 4h^2 < 2^22, h = (r-1)/2
 constexpr uint32_t kPermThreads = 256;
 constexpr uint32_t kRow1Threads = 128;
-constexpr uint32_t kDeriveThreads = 256;
+// 128 threads x <= 32 registers = 4096 registers per CTA: exactly what a
+// resident sieve CTA (768 x 80 = 61440 of 65536) leaves free, so the next
+// load's layout kernels run beside a sieve still in flight (the e2e pipeline)
+constexpr uint32_t kDeriveThreads = 128;
+constexpr uint32_t kDeriveMinBlocks = 16;
 constexpr uint32_t kDeriveItemWords = 2048;  // output words per k_derive CTA
 
 // ---- K2: sieve ---------------------------------------------------------------

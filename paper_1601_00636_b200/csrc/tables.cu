@@ -385,7 +385,7 @@ __global__ void __launch_bounds__(kPermThreads) k_permute(const PrimeJob* __rest
 // non-canonical loaded bytes. (Per-word gathers straight from L2 were
 // latency-bound: 113-145 us for the 256-prime set; a thread-strided staging
 // loop of word loads 29.9 us, 31% of it waiting on those loads.)
-__global__ void __launch_bounds__(kDeriveThreads) k_derive(const PrimeJob* __restrict__ jobs,
+__global__ void __launch_bounds__(kDeriveThreads, kDeriveMinBlocks) k_derive(const PrimeJob* __restrict__ jobs,
                                                            const uint4* __restrict__ items,
                                                            const uint8_t* __restrict__ packed,
                                                            uint32_t* __restrict__ ext,
@@ -508,7 +508,7 @@ __global__ void __launch_bounds__(kDeriveThreads) k_derive(const PrimeJob* __res
 // (prime r), row a = p mod r, offset b -- is the 32-q mask of that row at b
 // (bits u(a, (b + l) mod r)), and the entry index of the lane's next window
 // (a, (b + 1024) mod r). One thread per entry.
-__global__ void k_wintab(const uint4* __restrict__ probes, uint32_t nprobes, uint32_t entries,
+__global__ void __launch_bounds__(kDeriveThreads, kDeriveMinBlocks) k_wintab(const uint4* __restrict__ probes, uint32_t nprobes, uint32_t entries,
                          const uint32_t* __restrict__ ext, uint32_t stride, uint32_t* __restrict__ out)
 {
 	for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < entries; e += gridDim.x * blockDim.x) {
@@ -624,7 +624,8 @@ cudaError_t launch_wintab(const uint4* d_probes, uint32_t nprobes, uint32_t entr
                           uint32_t stride, uint32_t* d_out, cudaStream_t s)
 {
 	if (!entries) return cudaSuccess;
-	k_wintab<<<(entries + 255) / 256, 256, 0, s>>>(d_probes, nprobes, entries, d_ext, stride, d_out);
+	k_wintab<<<(entries + kDeriveThreads - 1) / kDeriveThreads, kDeriveThreads, 0, s>>>(d_probes, nprobes, entries,
+	                                                                                   d_ext, stride, d_out);
 	return cudaGetLastError();
 }
 
@@ -653,7 +654,7 @@ std::vector<uint4> derive_items(const std::vector<uint32_t>& primes)
 cudaError_t launch_load_check(const uint32_t* d_kf, const uint8_t* d_expect, uint32_t n, uint32_t* d_status,
                               cudaStream_t s)
 {
-	k_load_check<<<1, 256, 0, s>>>(d_kf, d_expect, n, d_status);
+	k_load_check<<<1, kDeriveThreads, 0, s>>>(d_kf, d_expect, n, d_status);
 	return cudaGetLastError();
 }
 
