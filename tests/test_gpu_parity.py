@@ -559,6 +559,30 @@ def test_files_roundtrip_with_reference(tmp_path, sets):
     assert empty.empty()
 
 
+def test_bench_subcommand_output(tmp_path, golden):
+    """cli.hpp:213-248 (cmd_bench) on the GPU: the reference default set's
+    files, REGION [152, 5000] -- 447,994,938 pairs per run (acceptance.cpp:
+    123-144), the reference's line formats and the paper's 3.54e-07 s/pair."""
+    import io
+    from paper_1601_00636_b200 import bench_cmd
+    s = cuboid.SieveSet.build_default()
+    tp, ip = str(tmp_path / "t.bin"), str(tmp_path / "p.bin")
+    s.save_files(tp, ip)
+    out = io.StringIO()
+    assert bench_cmd.cmd_bench(tp, ip, 152, 5000, 3, out=out) == 0
+    lines = out.getvalue().splitlines()
+    assert len(lines) == 5
+    for k in range(3):
+        assert lines[k].startswith(f"run {k + 1}: {golden['sieve']['R152_5000']['pairs_tested']} pairs in ")
+        assert lines[k].endswith(" s/pair")
+    assert lines[3] == "reference dt: 3.54e-07 s/pair"
+    assert lines[4].startswith("run-to-run variation: ")
+    out = io.StringIO()
+    bench_cmd.cmd_bench(tp, ip, 200, 199, 1, out=out)  # empty range
+    assert out.getvalue() == "run 1: 0 pairs in " + out.getvalue().split(" in ")[1]
+    assert out.getvalue().endswith(" s (empty range)\n")
+
+
 def test_dump_table_text_matches_u11():
     """test_sievetable.cpp:222-238: the text dump of r = 11 is the paper's U_11."""
     s = cuboid.SieveSet.build([2, 11])
