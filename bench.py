@@ -196,6 +196,33 @@ class CpuReference:
                     kind=self.kind, cores=self.cores)
 
 
+def reference_api_leg(args, wl, primes):
+    """C5 through the reference's own C++ API with the drop-in
+    (cpp/bench_dropin: cuboid::gpu::scan_triangle on a reference SieveSet,
+    results in the reference's ScanStats maps), tables resident and tables
+    re-uploaded from the host every call; the histogram is checked against
+    the reference golden. None when the binary was not built (it needs the
+    reference headers at build time)."""
+    exe = os.path.join(ROOT, "cpp", "_build", "bench_dropin")
+    if args.workload != "C5" or not os.path.exists(exe):
+        return None
+    r = subprocess.run([exe, str(args.steps), str(args.warmup)], capture_output=True, text=True, timeout=300)
+    if r.returncode != 0:
+        return {"error": r.stderr[-300:]}
+    d = json.loads(r.stdout.strip().splitlines()[-1])
+    path = os.path.join(ROOT, "tests", "golden", "golden.json")
+    g = json.load(open(path))["sieve"]["C5"]
+    ok = (d["pairs"] == g["pairs_tested"] and d["survivors"] == g["survivors"] and
+          d["kill_histogram"] == g["kill_histogram"] and d["blocks"] == len(g["block_r_max"]) and
+          d["same_both_legs"])
+    return {"path": "cuboid::gpu::scan_triangle(reference SieveSet, 100001, 300000) -> reference ScanStats",
+            "resident": {"value": d["pairs"] / d["resident_s"], "unit": "pairs/s", "ms_per_call": 1e3 * d["resident_s"]},
+            "upload_every_call": {"value": d["pairs"] / d["upload_s"], "unit": "pairs/s",
+                                  "ms_per_call": 1e3 * d["upload_s"],
+                                  "h2d_bytes_per_call": 25869968},
+            "parity": "ok" if ok else "MISMATCH", "steps": d["steps"]}
+
+
 def cpu_table_baseline(P256, tables_c2=None):
     """the reference's production build_table for all
     256 primes (1 thread and all cores) and its definition build_table_oracle
@@ -702,6 +729,7 @@ def run_ours(args, wl, primes):
                 "kind": s["kind"],
                 "sample": f"rows p={s['rows'][0]}..{s['rows'][1]} of {wl['desc'].split(':')[0]} "
                           f"({s['pairs']} pairs, {s['seconds']:.1f} s)"}
+            line["e2e_reference_api"] = reference_api_leg(args, wl, primes)
             s1 = CpuReference(wl, primes, 1).sample(args.cpu_budget / 2)
             line["cpu_baseline_1thread"] = {
                 "value": s1["pairs"] / s1["seconds"], "unit": "pairs/s", "cores": 1, "kind": s1["kind"],

