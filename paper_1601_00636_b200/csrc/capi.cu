@@ -9,6 +9,7 @@
 #include <fstream>
 #include <map>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/cuboid_gpu.h"
@@ -171,6 +172,11 @@ struct cgpu_ctx {
 	DevBuf<uint2> fprimes;
 	uint32_t n_fprimes = 0;
 
+	// pinned staging ring for uploads from pageable host memory (upload_pageable)
+	static constexpr size_t kStageBytes = size_t(4) << 20;
+	uint8_t* stage[2] = {nullptr, nullptr};
+	cudaEvent_t stage_ev[2] = {nullptr, nullptr};
+
 	// cooperative stop word (cgpu_set_stop_word): device view of a mapped host word
 	const volatile uint32_t* stop_dev = nullptr;
 
@@ -265,6 +271,10 @@ int cgpu_destroy(cgpu_ctx* c)
 	cudaStreamSynchronize(c->stream);
 	for (auto& e : c->ev)
 		if (e) cudaEventDestroy(e);
+	for (int i = 0; i < 2; ++i) {
+		if (c->stage[i]) cudaFreeHost(c->stage[i]);
+		if (c->stage_ev[i]) cudaEventDestroy(c->stage_ev[i]);
+	}
 	if (c->own_stream) cudaStreamDestroy(c->stream);
 	delete c;
 	return CGPU_OK;
@@ -592,6 +602,45 @@ int cgpu_tables_build(cgpu_ctx* c, const uint32_t* primes, uint32_t n, int algor
 	return CGPU_OK;
 }
 
+// Host -> device copy of `bytes` into the packed buffer. Pinned (or
+// registered) memory goes straight to the copy engine. Pageable memory -- a
+// reference SieveSet's std::vector, a file read -- would be staged by the
+// driver at a few GB/s; here it goes through two 4 MB pinned buffers, each
+// filled by several host threads while the copy engine drains the other.
+static int upload_host(cgpu_ctx* c, const void* bytes, uint64_t total)
+{
+	cudaPointerAttributes attr{};
+	const bool pinned = cudaPointerGetAttributes(&attr, bytes) == cudaSuccess &&
+	                    (attr.type == cudaMemoryTypeHost || attr.type == cudaMemoryTypeManaged);
+	cudaGetLastError();  // an unregistered pointer may leave an error behind on older drivers
+	if (pinned || total <= cgpu_ctx::kStageBytes) {
+		CK(cudaMemcpyAsync(c->packed.p, bytes, total, cudaMemcpyHostToDevice, c->stream));
+		return CGPU_OK;
+	}
+	for (int i = 0; i < 2; ++i) {
+		if (!c->stage[i]) CK(cudaMallocHost(&c->stage[i], cgpu_ctx::kStageBytes));
+		if (!c->stage_ev[i]) CK(cudaEventCreateWithFlags(&c->stage_ev[i], cudaEventDisableTiming));
+	}
+	const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+	const unsigned nt = std::min(4u, hw);
+	const uint8_t* src = static_cast<const uint8_t*>(bytes);
+	for (uint64_t off = 0, k = 0; off < total; off += cgpu_ctx::kStageBytes, ++k) {
+		const int b = static_cast<int>(k & 1);
+		const size_t len = static_cast<size_t>(std::min<uint64_t>(cgpu_ctx::kStageBytes, total - off));
+		CK(cudaEventSynchronize(c->stage_ev[b]));  // the copy that last read this buffer is done
+		const size_t per = (len + nt - 1) / nt;
+		std::vector<std::thread> th;
+		for (unsigned t = 1; t < nt; ++t)
+			if (t * per < len)
+				th.emplace_back([&, t] { std::memcpy(c->stage[b] + t * per, src + off + t * per, std::min(per, len - t * per)); });
+		std::memcpy(c->stage[b], src + off, std::min(per, len));
+		for (auto& x : th) x.join();
+		CK(cudaMemcpyAsync(c->packed.p + off, c->stage[b], len, cudaMemcpyHostToDevice, c->stream));
+		CK(cudaEventRecord(c->stage_ev[b], c->stream));
+	}
+	return CGPU_OK;
+}
+
 static int tables_load(cgpu_ctx* c, const uint32_t* primes, uint32_t n, const void* bytes, uint64_t nbytes,
                        cudaMemcpyKind kind, bool async = false);
 
@@ -650,7 +699,11 @@ static int tables_load(cgpu_ctx* c, const uint32_t* primes, uint32_t n, const vo
 	c->launches = 0;
 	if (n) {
 		if (!bytes) return set_err(CGPU_ERR_INVALID, "null table bytes");
-		CK(cudaMemcpyAsync(c->packed.p, bytes, total, kind, c->stream));
+		if (kind == cudaMemcpyHostToDevice) {
+			if (int rc = upload_host(c, bytes, total)) return rc;
+		} else {
+			CK(cudaMemcpyAsync(c->packed.p, bytes, total, kind, c->stream));
+		}
 		std::vector<uint32_t> eb;
 		uint64_t ew = 0;
 		std::vector<PrimeJob> jobs = make_jobs(c->primes, c->offsets, eb, ew);
