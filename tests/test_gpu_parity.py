@@ -6,6 +6,7 @@ bit-exact equality of tables, pair counts, first-killer histograms, block
 r_max and survivor lists."""
 from __future__ import annotations
 
+import ctypes as C
 import hashlib
 import random
 
@@ -531,6 +532,61 @@ def test_async_loads_verified_on_the_device(dev, golden, sets):
     o = port.sieve(bytes(w0), P, offs, 2, 3000, port.TRIANGLE)
     assert (r.pairs_tested, r.survivors) == (o["pairs_tested"], o["survivors"])
     assert r.hist.tolist() == o["hist"].tolist()
+
+
+def test_in_process_multi_gpu_clique(golden, sets):
+    """cgpu_multi_* (the in-process NCCL path of cuboid::gpu::scan(...,
+    devices)) over every device this box has: C3 whole-row TRIANGLE and a
+    REGION span ending mid-row equal the reference's / the single-context
+    result; survivors gathered in canonical order (weak sieve)."""
+    L = N.lib()
+    n = C.c_int()
+    N.check(L.cgpu_device_count(C.byref(n)))
+    devs = (C.c_int * n.value)(*range(n.value))
+    m = C.c_void_p()
+    N.check(L.cgpu_multi_create(n.value, devs, C.byref(m)))
+    try:
+        def run(P, lo, q0, hi, q_end, mode, cap=1 << 16):
+            pr = np.ascontiguousarray(P, dtype=np.uint32)
+            tb, _ = port.build_set(P)
+            buf = np.frombuffer(tb, np.uint8)
+            N.check(L.cgpu_multi_tables_load(m, pr.ctypes.data_as(C.c_void_p), len(pr),
+                                             buf.ctypes.data_as(C.c_void_p), len(tb)))
+            counts = np.zeros(2, np.uint64)
+            hist = np.zeros(len(P), np.uint64)
+            nb = hi // 100 - lo // 100 + 1
+            brm = np.zeros(nb, np.uint32)
+            surv = np.zeros((cap, 2), np.uint64)
+            N.check(L.cgpu_multi_sieve(m, lo, q0, hi, q_end, mode, counts.ctypes.data_as(C.c_void_p),
+                                       hist.ctypes.data_as(C.c_void_p), brm.ctypes.data_as(C.c_void_p), nb,
+                                       surv.ctypes.data_as(C.c_void_p), cap))
+            return counts, hist, brm, surv[:int(counts[1])]
+        P = sets["odd64"]
+        counts, hist, brm, _ = run(P, 2, 0, 10000, 0, N.TRIANGLE)
+        g = golden["sieve"]["C3"]
+        assert (int(counts[0]), int(counts[1])) == (g["pairs_tested"], g["survivors"])
+        assert {str(P[k]): int(c) for k, c in enumerate(hist) if c} == g["kill_histogram"]
+        assert {str(i): int(v) for i, v in enumerate(brm) if v} == g["block_r_max"]
+        W = [11]
+        counts, hist, brm, surv = run(W, 1, 1, 40, 0, N.REGION)
+        tb, offs = port.build_set(W)
+        o = port.sieve(tb, W, offs, 1, 40, port.REGION, q_start=1)
+        assert (int(counts[0]), int(counts[1])) == (o["pairs_tested"], o["survivors"])
+        assert np.array_equal(surv, o["survivor_pairs"])
+        D = default_primes()
+        counts, hist, brm, _ = run(D, 152, 3, 700, 12345, N.REGION)  # ends mid-row 700, at q = 12345
+        # the reference halted at (700, 12346): a pre-armed stop at that q visited
+        visited = 1 + sum(cuboid.q_bounds(p)[1] - (3 if p == 152 else cuboid.q_bounds(p)[0]) + 1
+                          for p in range(152, 700)) + (12346 - cuboid.q_bounds(700)[0])
+        rs = refmod.RefSet.build(D)
+        ref = refmod.scan(rs, 152, 3, 700, batch_pairs=visited, stop_preset=True)
+        assert ref.stopped and (ref.resume_p, ref.resume_q) == (700, 12346)
+        assert (int(counts[0]), int(counts[1])) == (ref.pairs_tested, ref.survivors)
+        assert [int(x) for x in hist] == list(ref.hist_by_rank)
+        got_brm = {152 // 100 + i: int(v) for i, v in enumerate(brm) if v}
+        assert got_brm == ref.block_r_max
+    finally:
+        L.cgpu_multi_destroy(m)
 
 
 def test_files_roundtrip_with_reference(tmp_path, sets):
