@@ -589,6 +589,62 @@ def test_in_process_multi_gpu_clique(golden, sets):
         L.cgpu_multi_destroy(m)
 
 
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_random_region_spans_vs_reference(dev, seed):
+    """Seeded REGION spans that start AND end mid-row (cgpu_sieve_span, what a
+    stopped scan covers) against the reference's own scan() halted by a
+    pre-armed stop at the same pair (engine.hpp:248-257): counts, histogram,
+    block r_max."""
+    rng = random.Random(seed)
+    D = default_primes()
+    tb, _ = port.build_set(D)
+    dev.load(D, tb)
+    rs = refmod.RefSet.build(D)
+    for _ in range(6):
+        p0 = rng.randrange(152, 20000)
+        lo, hi = cuboid.q_bounds(p0)
+        q0 = rng.randrange(lo, hi + 1)
+        p1 = p0 + rng.randrange(0, 40)
+        lo1, hi1 = cuboid.q_bounds(p1)
+        q1 = rng.randrange(lo1 if p1 > p0 else q0, hi1 + 1)  # last pair sieved
+        visited = 1 + sum(cuboid.q_bounds(p)[1] - (q0 if p == p0 else cuboid.q_bounds(p)[0]) + 1
+                          for p in range(p0, p1)) + (q1 + 1 - (q0 if p1 == p0 else lo1))
+        stop_at = cuboid.region_advance((p0, q0), visited - 1, p1 + 1)
+        assert stop_at == ((p1, q1 + 1) if q1 < hi1 else (p1 + 1, cuboid.q_bounds(p1 + 1)[0]))
+        ref = refmod.scan(rs, p0, q0, p1 + 1, batch_pairs=visited, stop_preset=True)
+        assert ref.stopped and (ref.resume_p, ref.resume_q) == stop_at
+        nb = p1 // 100 - p0 // 100 + 1
+        counts = np.zeros(2, np.uint64)
+        hist = np.zeros(len(D), np.uint64)
+        brm = np.zeros(nb, np.uint32)
+        spq = np.zeros((16, 2), np.uint64)
+        N.check(N.lib().cgpu_sieve_span(dev._ctx, p0, q0, p1, q1, counts.ctypes.data_as(C.c_void_p),
+                                        hist.ctypes.data_as(C.c_void_p), brm.ctypes.data_as(C.c_void_p), nb,
+                                        spq.ctypes.data_as(C.c_void_p), 16))
+        assert (int(counts[0]), int(counts[1])) == (ref.pairs_tested, ref.survivors)
+        assert [int(x) for x in hist] == list(ref.hist_by_rank)
+        got = {p0 // 100 + i: int(v) for i, v in enumerate(brm) if v}
+        # the reference also enters the stop row's block, which lies past the span
+        # when the stop is the first pair of row p1 + 1
+        want = {b: r for b, r in ref.block_r_max.items() if b <= p1 // 100}
+        assert got == want
+
+
+def test_classify_large_pairs_vs_reference(dev, sets):
+    """k_classify's 64-bit residues for pairs up to 2^32 against the
+    reference's SieveSet::is_unsolvable in rank order."""
+    P = sets["odd256"]
+    tb, _ = port.build_set(P)
+    dev.load(P, tb)
+    rng = np.random.default_rng(99)
+    p = rng.integers(1 << 20, (1 << 32) - 1, 20000, dtype=np.uint64)
+    q = rng.integers(1, 1 << 32, 20000, dtype=np.uint64)
+    pq = np.stack([p, q], 1)
+    got = dev.classify(pq)
+    want = refmod.classify(refmod.RefSet.build(P), pq, 4)
+    assert np.array_equal(got.astype(np.int64), want.astype(np.int64))
+
+
 def test_files_roundtrip_with_reference(tmp_path, sets):
     """GPU-built tables written through the C ABI are the reference's files
     (save_sieve_files / load_sieve_files, test_sievetable.cpp:240-262), and
