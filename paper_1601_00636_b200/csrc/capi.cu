@@ -169,6 +169,7 @@ struct cgpu_ctx {
 
 	uint32_t row_cost = kDefaultRowCost;
 	float drain_alpha = kDefaultDrainAlpha;
+	int short_rows = -1;  // CUBOID_SHORT_ROWS: -1 by mean row length, 0 / 1 forced
 	DevBuf<uint2> fprimes;
 	uint32_t n_fprimes = 0;
 
@@ -242,6 +243,7 @@ int cgpu_create(int device, void* stream, cgpu_ctx** out)
 	cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device);
 	if (const char* rc = std::getenv("CUBOID_ROW_COST")) c->row_cost = static_cast<uint32_t>(std::atoi(rc));
 	if (const char* da = std::getenv("CUBOID_DRAIN_ALPHA")) c->drain_alpha = static_cast<float>(std::atof(da));
+	if (const char* sr = std::getenv("CUBOID_SHORT_ROWS")) c->short_rows = std::atoi(sr) < 0 ? -1 : (std::atoi(sr) ? 1 : 0);
 	for (auto& e : c->ev) cudaEventCreate(&e);
 	// trial-division primes below 2^16 (covers sqrt of any p < 2^32)
 	std::vector<uint2> fp;
@@ -953,6 +955,12 @@ int enqueue_sieve(cgpu_ctx* c, uint64_t p_lo, uint64_t q_start, uint64_t p_hi, u
 	a.n_fprimes = c->n_fprimes;
 	a.row_cost = c->row_cost;
 	a.drain_alpha = c->drain_alpha;
+	{  // mean windows per row of the launch: TRIANGLE rows hold ~p q, REGION rows ~59p
+		const double pm = 0.5 * (static_cast<double>(p_lo) + static_cast<double>(p_hi));
+		const double mean_windows = (mode == CGPU_TRIANGLE ? pm : 59.0 * pm) / 32.0;
+		a.short_rows = c->short_rows < 0 ? (mean_windows < kShortRowWindows ? 1u : 0u)
+		                                 : static_cast<uint32_t>(c->short_rows);
+	}
 	a.p_lo = p_lo;
 	a.p_hi = p_hi;
 	a.q_start = q_start;

@@ -85,6 +85,9 @@ constexpr int kSieveThreads = CGPU_SIEVE_THREADS;
 #define CGPU_SIEVE_MIN_BLOCKS 1
 #endif
 constexpr int kSieveMinBlocks = CGPU_SIEVE_MIN_BLOCKS;  // CTAs per SM the register budget targets
+// Launches whose mean row has fewer windows run the short-row kernel variant
+// (dispatch_row SHORT): C4's rows average 1.6k windows, C5's 6.3k.
+constexpr uint32_t kShortRowWindows = 4000;
 constexpr uint32_t kDefaultRowCost = 800;                 // window-equivalents per row setup (measured: 500 -> 800 C4 -2%, C5 -0.5%)
 constexpr int kSieveWarps = kSieveThreads / 32;
 constexpr int kMaxReg2 = 8;     // leading probes held in registers with r <= 31 (2-word rows)
@@ -146,6 +149,7 @@ struct SieveArgs {
 	uint32_t n_slots;
 	uint32_t row_cost;            // load-balance charge per row (window-equivalents)
 	float drain_alpha;            // load-balance weight of a window queued for the deep probes
+	uint32_t short_rows;          // run the short-row loop-variant set (standard-prime kernel)
 	// work units before slot s = prefix[s] + chunk_off[s / kPlanChunk]
 	unsigned long long* prefix;        // [n_slots + 1] (chunk-local exclusive scan)
 	unsigned long long* chunk_off;     // [n_chunks + 1] (exclusive scan of chunk totals)

@@ -613,7 +613,7 @@ __device__ __forceinline__ uint32_t row_loop(const SieveArgs& a, const WarpSmem&
 	return kmax;
 }
 
-template <int NR2, int NR3, bool STD>
+template <int NR2, int NR3, bool STD, bool SHORT>
 __device__ __forceinline__ uint32_t dispatch_row(const SieveArgs& a, const WarpSmem& w, uint32_t lane,
                                                  const RowCtx& rc)
 {
@@ -621,15 +621,25 @@ __device__ __forceinline__ uint32_t dispatch_row(const SieveArgs& a, const WarpS
 	// slots (padding slots cost 4 instructions per window). Fewer copies of
 	// the loop keep the kernel in the instruction cache when consecutive rows
 	// differ in their factor count (C5: 60% of the work has <= 2 odd factors,
-	// 32% has 3, 8% has 4-5).
-	switch (rc.nf) {
-	case 0:
-	case 1:
-	case 2: return row_loop<NR2, NR3, STD, 2>(a, w, lane, rc);
-	case 3: return row_loop<NR2, NR3, STD, 3>(a, w, lane, rc);
-	case 4:
-	case 5: return row_loop<NR2, NR3, STD, 5>(a, w, lane, rc);
-	default: return row_loop<NR2, NR3, STD, 9>(a, w, lane, rc);
+	// 32% has 3, 8% has 4-5). SHORT (launches of short rows, where a warp
+	// switches rows every few hundred windows and instruction fetch binds --
+	// C4: 28% of the stall samples): three, {2, 4, 9} slots. Measured against
+	// the four (r02p_variants_ab.txt): C3 -8%, C4 -13%, TRIANGLE p <= 5e4 -16%,
+	// 5e4 < p <= 1.5e5 -7%; 1e5 < p <= 2e5 +1%, C5 +5%.
+	if constexpr (SHORT) {
+		if (rc.nf <= 2) return row_loop<NR2, NR3, STD, 2>(a, w, lane, rc);
+		if (rc.nf <= 4) return row_loop<NR2, NR3, STD, 4>(a, w, lane, rc);
+		return row_loop<NR2, NR3, STD, 9>(a, w, lane, rc);
+	} else {
+		switch (rc.nf) {
+		case 0:
+		case 1:
+		case 2: return row_loop<NR2, NR3, STD, 2>(a, w, lane, rc);
+		case 3: return row_loop<NR2, NR3, STD, 3>(a, w, lane, rc);
+		case 4:
+		case 5: return row_loop<NR2, NR3, STD, 5>(a, w, lane, rc);
+		default: return row_loop<NR2, NR3, STD, 9>(a, w, lane, rc);
+		}
 	}
 }
 
@@ -640,7 +650,7 @@ __device__ unsigned long long g_wclk[3 * 8192];
 // STOP: polls the cooperative stop word (SieveArgs::stop). The standard-prime
 // kernel, the benchmarked one, also exists without the poll: even a per-row
 // test of a kernel parameter moved its code layout and cost it ~6% (C5).
-template <int NR2, int NR3, bool STD, bool STOP = true>
+template <int NR2, int NR3, bool STD, bool STOP = true, bool SHORT = false>
 __global__ void __launch_bounds__(kSieveThreads, kSieveMinBlocks) k_sieve(const SieveArgs a)
 {
 	constexpr int NREG = NR2 + NR3;
@@ -754,7 +764,7 @@ __global__ void __launch_bounds__(kSieveThreads, kSieveMinBlocks) k_sieve(const 
 		}
 		__syncwarp();
 
-		const uint32_t kk = dispatch_row<NR2, NR3, STD>(a, w, lane, rc);  // 1 + deepest killer
+		const uint32_t kk = dispatch_row<NR2, NR3, STD, SHORT>(a, w, lane, rc);  // 1 + deepest killer
 		if (lane == 0 && kk) {
 			const uint32_t j = kk - 1;
 			uint32_t killer;
@@ -841,18 +851,22 @@ __global__ void k_classify(const uint64_t* __restrict__ pq, uint64_t n,
 	}
 }
 
-template <int NR2, int NR3, bool STD = false, bool STOP = true>
+template <int NR2, int NR3, bool STD = false, bool STOP = true, bool SHORT = false>
 void* sieve_fn()
 {
-	return reinterpret_cast<void*>(&k_sieve<NR2, NR3, STD, STOP>);
+	return reinterpret_cast<void*>(&k_sieve<NR2, NR3, STD, STOP, SHORT>);
 }
 
 // Instantiated: NR2 in 0..8 with NR3 = 0, and NR2 = 7 (every prime 11..31
 // killable -- all BASELINE sets) with NR3 in 1..kMaxReg3; the standard-prime
-// kernel with and without the stop poll.
-void* sieve_kernel_ptr(int nr2, int nr3, bool std_primes, bool stop = true)
+// kernel with and without the stop poll, each with the long- and short-row
+// loop-variant sets.
+void* sieve_kernel_ptr(int nr2, int nr3, bool std_primes, bool stop = true, bool short_rows = false)
 {
-	if (std_primes) return stop ? sieve_fn<7, 1, true, true>() : sieve_fn<7, 1, true, false>();
+	if (std_primes) {
+		if (short_rows) return stop ? sieve_fn<7, 1, true, true, true>() : sieve_fn<7, 1, true, false, true>();
+		return stop ? sieve_fn<7, 1, true, true>() : sieve_fn<7, 1, true, false>();
+	}
 	if (nr2 == 7 && nr3 > 0) {
 		switch (nr3) {
 		case 1: return sieve_fn<7, 1>();
@@ -892,7 +906,9 @@ int sieve_grid(int device, int nr2, int nr3, bool std_primes, size_t smem)
 	// per-launch-size attribute set for one would reject another's launch.
 	int optin = 0;
 	cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
-	const void* variants[2] = {fn, sieve_kernel_ptr(nr2, nr3, std_primes, false)};
+	const void* variants[4] = {fn, sieve_kernel_ptr(nr2, nr3, std_primes, false),
+	                           sieve_kernel_ptr(nr2, nr3, std_primes, true, true),
+	                           sieve_kernel_ptr(nr2, nr3, std_primes, false, true)};
 	for (const void* f : variants) {
 		cudaFuncAttributes fa{};
 		cudaFuncGetAttributes(&fa, f);
@@ -915,7 +931,7 @@ cudaError_t launch_sieve(const SieveArgs& a, int grid, cudaStream_t s)
 	const size_t smem = sieve_smem_bytes(a.np, a.wtab_n ? (a.std_primes ? kTabStrideStd : kTabStrideGen) : 0);
 	void* args[] = {const_cast<SieveArgs*>(&a)};
 	return cudaLaunchKernel(sieve_kernel_ptr(static_cast<int>(a.nreg2), static_cast<int>(a.nreg3), a.std_primes,
-	                                         a.stop != nullptr),
+	                                         a.stop != nullptr, a.short_rows != 0),
 	                        dim3(grid),
 	                        dim3(kSieveThreads), args, smem, s);
 }

@@ -11,15 +11,18 @@ CHILD = r'''
 import sys, os, json
 sys.path.insert(0, os.environ["ROOT"])
 from paper_1601_00636_b200 import device as D, _native as N, odd_primes
-cfg = {"C3": (64, 2, 10000), "C4": (128, 2, 100000), "C5": (256, 100001, 300000)}
+cfg = {"C3": (64, 2, 10000), "C4": (128, 2, 100000), "C5": (256, 100001, 300000),
+       "T50k": (256, 2, 50000), "T150k": (256, 50001, 150000), "T200k": (256, 100001, 200000),
+       "R5k": (96, 152, 5000)}
 dev = D.Device(0)
 out = {}
 for name in sys.argv[1].split(","):
     k, lo, hi = cfg[name]
     dev.build(odd_primes(k), N.BUILD_PRODUCTION, download=False)
     t = []
+    mode = N.REGION if name.startswith("R") else N.TRIANGLE
     for _ in range(5):
-        r = dev.sieve(lo, hi, N.TRIANGLE)
+        r = dev.sieve(lo, hi, mode)
         t.append(dev.timings_ms()["sieve"])
     out[name] = (min(t[1:]), r.pairs_tested)
 print(json.dumps(out))
