@@ -168,6 +168,7 @@ struct cgpu_ctx {
 	std::map<uint64_t, int> grid_cache;
 
 	uint32_t row_cost = kDefaultRowCost;
+	uint32_t row_cost_short = kDefaultRowCostShort;
 	float drain_alpha = kDefaultDrainAlpha;
 	int short_rows = -1;  // CUBOID_SHORT_ROWS: -1 by mean row length, 0 / 1 forced
 	DevBuf<uint2> fprimes;
@@ -242,6 +243,8 @@ int cgpu_create(int device, void* stream, cgpu_ctx** out)
 	}
 	cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device);
 	if (const char* rc = std::getenv("CUBOID_ROW_COST")) c->row_cost = static_cast<uint32_t>(std::atoi(rc));
+	if (const char* rs = std::getenv("CUBOID_ROW_COST_SHORT"))
+		c->row_cost_short = static_cast<uint32_t>(std::atoi(rs));
 	if (const char* da = std::getenv("CUBOID_DRAIN_ALPHA")) c->drain_alpha = static_cast<float>(std::atof(da));
 	if (const char* sr = std::getenv("CUBOID_SHORT_ROWS")) c->short_rows = std::atoi(sr) < 0 ? -1 : (std::atoi(sr) ? 1 : 0);
 	for (auto& e : c->ev) cudaEventCreate(&e);
@@ -960,6 +963,7 @@ int enqueue_sieve(cgpu_ctx* c, uint64_t p_lo, uint64_t q_start, uint64_t p_hi, u
 		const double mean_windows = (mode == CGPU_TRIANGLE ? pm : 59.0 * pm) / 32.0;
 		a.short_rows = c->short_rows < 0 ? (mean_windows < kShortRowWindows ? 1u : 0u)
 		                                 : static_cast<uint32_t>(c->short_rows);
+		if (a.short_rows) a.row_cost = c->row_cost_short;  // the short-row kernel's own setup charge
 	}
 	a.p_lo = p_lo;
 	a.p_hi = p_hi;

@@ -88,6 +88,7 @@ constexpr int kSieveMinBlocks = CGPU_SIEVE_MIN_BLOCKS;  // CTAs per SM the regis
 // Launches whose mean row has fewer windows run the short-row kernel variant
 // (dispatch_row SHORT): C4's rows average 1.6k windows, C5's 6.3k.
 constexpr uint32_t kShortRowWindows = 4000;
+constexpr uint32_t kDefaultRowCostShort = 650;  // ... for the short-row kernel (sweep: C4 0.528 -> 0.521 ms)
 constexpr uint32_t kDefaultRowCost = 800;                 // window-equivalents per row setup (measured: 500 -> 800 C4 -2%, C5 -0.5%)
 constexpr int kSieveWarps = kSieveThreads / 32;
 constexpr int kMaxReg2 = 8;     // leading probes held in registers with r <= 31 (2-word rows)
