@@ -202,6 +202,24 @@ int main()
 		CHECK(same(g, r));
 	}
 
+	// the deferred residency check: a different set of the same shape (one
+	// table byte changed) scanned right after -- detected while the device
+	// sieves, uploaded, sieved again
+	{
+		std::vector<uint8_t> t = gpu_default.tables();
+		std::vector<PrimeRecord> idx = gpu_default.index();
+		t[idx[3].offset + 5] ^= 0x10;  // a bit of row >= 1 of the 4th table (r = 19), not padding
+		const SieveSet edited = SieveSet::from_parts(idx, t);
+		const ScanStats g0 = gpu::scan(gpu_default, {152, 3}, 900);
+		const ScanStats g1 = gpu::scan(edited, {152, 3}, 900);
+		const ScanStats g2 = gpu::scan(gpu_default, {152, 3}, 900);
+		CHECK(same(g0, scan(ref_default, {152, 3}, 900)));
+		CHECK(same(g1, scan(edited, {152, 3}, 900)));
+		CHECK(same(g2, g0));
+		CHECK(!same(g1, g0));
+		CHECK(same(gpu::scan_triangle(edited, 2, 700), ref_triangle(edited, 2, 700, nullptr)));
+	}
+
 	// building another set replaces the context's tables; the next
 	// scan of the first set must upload it again (and size its histogram by it)
 	{

@@ -112,12 +112,20 @@ inline bool equal_bytes(const uint8_t* a, const uint8_t* b, size_t n)
 // edited load_sieve file allocated at a freed set's address.
 class Residency {
 public:
-	bool holds(const SieveSet& set, std::vector<uint32_t>& primes) const
+	// same prime list and byte count as the resident set (fills `primes`)
+	bool same_shape(const SieveSet& set, std::vector<uint32_t>& primes) const
 	{
 		primes.clear();
 		for (const PrimeRecord& r : set.index()) primes.push_back(r.prime);
-		return valid_ && primes == primes_ && set.tables().size() == bytes_.size() &&
-		       detail::equal_bytes(set.tables().data(), bytes_.data(), bytes_.size());
+		return valid_ && primes == primes_ && set.tables().size() == bytes_.size();
+	}
+	bool same_bytes(const SieveSet& set) const
+	{
+		return detail::equal_bytes(set.tables().data(), bytes_.data(), bytes_.size());
+	}
+	bool holds(const SieveSet& set, std::vector<uint32_t>& primes) const
+	{
+		return same_shape(set, primes) && same_bytes(set);
 	}
 	void record(const SieveSet& set, std::vector<uint32_t>&& primes)
 	{
@@ -149,28 +157,65 @@ public:
 	cgpu_ctx* span_ctx() { return ctx_; }
 	int device() const { return device_; }
 
-	// Makes `set` resident unless it already is.
-	void ensure_resident(const SieveSet& set)
+	// Makes `set` resident unless it already is. defer: when the resident set
+	// has the same primes and size, the byte comparison (~1 ms for 26 MB on
+	// the host) is left to the next sieve(), which runs it while the device
+	// sieves and, on a mismatch, uploads the set and sieves again.
+	void ensure_resident(const SieveSet& set, bool defer = false)
 	{
+		verify_ = nullptr;
 		std::vector<uint32_t> primes;
-		if (res_.holds(set, primes)) return;
-		res_.invalidate();
-		check(cgpu_tables_load(ctx_, primes.data(), static_cast<uint32_t>(primes.size()),
-		                       set.tables().data(), set.tables().size()),
-		      "cgpu_tables_load");
-		res_.record(set, std::move(primes));
+		if (res_.same_shape(set, primes)) {
+			if (defer) {
+				verify_ = &set;
+				return;
+			}
+			if (res_.same_bytes(set)) return;
+		}
+		upload(set, std::move(primes));
 	}
-	void invalidate() { res_.invalidate(); }
+	void invalidate()
+	{
+		res_.invalidate();
+		verify_ = nullptr;
+	}
 
 	int sieve(uint64_t p_lo, uint64_t q_start, uint64_t p_hi, int mode, uint64_t* counts, uint64_t* hist,
 	          uint32_t* brm, uint64_t nb, uint64_t* surv, uint64_t cap)
 	{
-		return cgpu_sieve(ctx_, p_lo, q_start, p_hi, mode, 1, 0, counts, hist, brm, nb, surv, cap);
+		if (!verify_) return cgpu_sieve(ctx_, p_lo, q_start, p_hi, mode, 1, 0, counts, hist, brm, nb, surv, cap);
+		const SieveSet* s = verify_;
+		verify_ = nullptr;
+		int rc = cgpu_sieve_launch(ctx_, p_lo, q_start, p_hi, mode, 1, 0, surv ? cap : 0);
+		const bool same = res_.same_bytes(*s);  // on the host while the device sieves
+		if (!same) {  // another set of the same shape: discard, upload it, sieve again
+			cgpu_synchronize(ctx_);
+			std::vector<uint32_t> primes;
+			for (const PrimeRecord& r : s->index()) primes.push_back(r.prime);
+			upload(*s, std::move(primes));
+			rc = cgpu_sieve_launch(ctx_, p_lo, q_start, p_hi, mode, 1, 0, surv ? cap : 0);
+		}
+		if (rc != CGPU_OK) return rc;
+		return cgpu_sieve_results(ctx_, counts, hist, brm, nb, surv, cap);
 	}
 	int sieve_span(uint64_t p_lo, uint64_t q_start, uint64_t p_hi, uint64_t q_end, uint64_t* counts,
 	               uint64_t* hist, uint32_t* brm, uint64_t nb, uint64_t* surv, uint64_t cap)
 	{
+		settle();
 		return cgpu_sieve_span(ctx_, p_lo, q_start, p_hi, q_end, counts, hist, brm, nb, surv, cap);
+	}
+	void drop_deferred() { verify_ = nullptr; }  // the check is redone by the next scan
+	// completes a deferred residency check before a synchronous call
+	void settle()
+	{
+		if (!verify_) return;
+		const SieveSet* s = verify_;
+		verify_ = nullptr;
+		if (!res_.same_bytes(*s)) {
+			std::vector<uint32_t> primes;
+			for (const PrimeRecord& r : s->index()) primes.push_back(r.prime);
+			upload(*s, std::move(primes));
+		}
 	}
 	void set_stop_word(uint32_t* w) { check(cgpu_set_stop_word(ctx_, w), "cgpu_set_stop_word"); }
 	uint32_t loaded_primes()
@@ -183,9 +228,19 @@ public:
 	std::recursive_mutex& mutex() { return mu_; }
 
 private:
+	void upload(const SieveSet& set, std::vector<uint32_t>&& primes)
+	{
+		res_.invalidate();
+		check(cgpu_tables_load(ctx_, primes.data(), static_cast<uint32_t>(primes.size()),
+		                       set.tables().data(), set.tables().size()),
+		      "cgpu_tables_load");
+		res_.record(set, std::move(primes));
+	}
+
 	int device_;
 	cgpu_ctx* ctx_ = nullptr;
 	Residency res_;
+	const SieveSet* verify_ = nullptr;  // a deferred byte comparison (ensure_resident(set, true))
 	std::recursive_mutex mu_;
 };
 
@@ -214,7 +269,8 @@ public:
 		return c;
 	}
 
-	void ensure_resident(const SieveSet& set)
+	void drop_deferred() {}
+	void ensure_resident(const SieveSet& set, bool /*defer*/ = false)
 	{
 		std::vector<uint32_t> primes;
 		if (res_.holds(set, primes)) return;
@@ -498,7 +554,7 @@ ScanStats scan_on(Ctx& c, const SieveSet& set, SearchPair start, uint64_t p_end,
 	st.resume_q = start.q;
 	const auto t0 = std::chrono::steady_clock::now();
 	std::lock_guard<std::recursive_mutex> lk(c.mutex());
-	c.ensure_resident(set);
+	c.ensure_resident(set, /*defer=*/true);  // byte check overlapped with the first sieve
 	auto publish = [&](uint64_t p, uint64_t q) {  // flush_hooks (engine.hpp:218-223)
 		if (opt.hooks.current_p) opt.hooks.current_p->store(p, std::memory_order_relaxed);
 		if (opt.hooks.current_q) opt.hooks.current_q->store(q, std::memory_order_relaxed);
@@ -515,6 +571,7 @@ ScanStats scan_on(Ctx& c, const SieveSet& set, SearchPair start, uint64_t p_end,
 	};
 
 	if (start.p > p_end) {  // the reference's row loop does not run
+		c.drop_deferred();
 		st.elapsed = std::chrono::steady_clock::now() - t0;
 		return st;
 	}
@@ -612,7 +669,7 @@ inline ScanStats scan_triangle(const SieveSet& set, uint64_t p_lo, uint64_t p_hi
 	if (p_lo <= p_hi) {
 		auto go = [&](auto& c) {
 			std::lock_guard<std::recursive_mutex> lk(c.mutex());
-			c.ensure_resident(set);
+			c.ensure_resident(set, /*defer=*/true);
 			detail::fold(set, detail::run(c, set, p_lo, 0, p_hi, CGPU_TRIANGLE), st, sink);
 		};
 		if (devices.size() > 1)
