@@ -164,6 +164,12 @@ struct cgpu_ctx {
 	DevBuf<uint4> d_tabprobes;
 	DevBuf<uint4> derive_items;
 	DevBuf<uint32_t> wintab;
+	// wheel sieve (k_wsieve) for the standard probe sets: CUBOID_WHEEL=0 keeps k_sieve
+	bool wheel_enabled = true, wheel = false;
+	DevBuf<uint32_t> wheeltab;
+	int wgrid = 0;
+	uint32_t row_cost_wheel = kDefaultRowCostWheel;
+	float drain_alpha_wheel = kDefaultDrainAlphaWheel;
 	int grid = 0;
 	std::map<uint64_t, int> grid_cache;
 
@@ -246,6 +252,9 @@ int cgpu_create(int device, void* stream, cgpu_ctx** out)
 	if (const char* rs = std::getenv("CUBOID_ROW_COST_SHORT"))
 		c->row_cost_short = static_cast<uint32_t>(std::atoi(rs));
 	if (const char* da = std::getenv("CUBOID_DRAIN_ALPHA")) c->drain_alpha = static_cast<float>(std::atof(da));
+	if (const char* wh = std::getenv("CUBOID_WHEEL")) c->wheel_enabled = std::atoi(wh) != 0;
+	if (const char* rw = std::getenv("CUBOID_ROW_COST_WHEEL")) c->row_cost_wheel = static_cast<uint32_t>(std::atoi(rw));
+	if (const char* aw = std::getenv("CUBOID_DRAIN_ALPHA_WHEEL")) c->drain_alpha_wheel = static_cast<float>(std::atof(aw));
 	if (const char* sr = std::getenv("CUBOID_SHORT_ROWS")) c->short_rows = std::atoi(sr) < 0 ? -1 : (std::atoi(sr) ? 1 : 0);
 	for (auto& e : c->ev) cudaEventCreate(&e);
 	// trial-division primes below 2^16 (covers sqrt of any p < 2^32)
@@ -469,6 +478,14 @@ int finalize_set(cgpu_ctx* c, bool check_padding = false, bool keep_row0 = false
 		c->std_primes = c->nreg2 == 7 && c->nreg3 == static_cast<uint32_t>(kStdReg3) &&
 		                !std::getenv("CUBOID_NO_STD_PRIMES");
 		for (uint32_t j = 0; c->std_primes && j < c->nreg; ++j) c->std_primes = c->reg_r[j] == std_prime(j);
+	}
+	// k_wsieve needs the standard register probes and its shared memory (larger sets keep k_sieve)
+	c->wheel = c->std_primes && c->wheel_enabled && wsieve_smem_bytes(c->np) <= 220 * 1024;
+	if (c->wheel) {  // wheel tables (11, 13, 17 as the wheel; strided window tables of 19..37)
+		CK(c->wheeltab.ensure(kWtWords));
+		CK(launch_wheeltab(c->ext.p, c->reg_base, c->wheeltab.p, c->stream));
+		++c->launches;
+		if (!c->wgrid) c->wgrid = wsieve_grid(c->device, wsieve_smem_bytes(c->np));
 	}
 	const size_t smem =
 	    sieve_smem_bytes(c->np, c->wtab_n ? (c->std_primes ? kTabStrideStd : kTabStrideGen) : 0);
@@ -965,6 +982,12 @@ int enqueue_sieve(cgpu_ctx* c, uint64_t p_lo, uint64_t q_start, uint64_t p_hi, u
 		                                 : static_cast<uint32_t>(c->short_rows);
 		if (a.short_rows) a.row_cost = c->row_cost_short;  // the short-row kernel's own setup charge
 	}
+	a.wheel = c->wheel ? 1u : 0u;
+	a.wheeltab = c->wheeltab.p;
+	if (a.wheel) {
+		a.row_cost = c->row_cost_wheel;
+		a.drain_alpha = c->drain_alpha_wheel;
+	}
 	a.p_lo = p_lo;
 	a.p_hi = p_hi;
 	a.q_start = q_start;
@@ -1012,7 +1035,7 @@ int enqueue_sieve(cgpu_ctx* c, uint64_t p_lo, uint64_t q_start, uint64_t p_hi, u
 			CK(launch_plan(a, c->stream));
 			if (!ev1) CK(cudaEventRecord(c->ev[1], c->stream));  // sieve time excludes the first plan
 			ev1 = true;
-			CK(launch_sieve(a, c->grid, c->stream));
+			CK(launch_sieve(a, a.wheel ? c->wgrid : c->grid, c->stream));
 			c->launches += 2;
 		}
 	}

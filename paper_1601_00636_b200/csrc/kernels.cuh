@@ -125,6 +125,40 @@ constexpr uint32_t kPlanChunk = 1024;  // row slots per plan CTA
 constexpr uint32_t kFacWords = 1 + 2 * kMaxFactors;
 constexpr float kDefaultDrainAlpha = 12.0f;
 
+// ---- K2w: the wheel sieve (k_wsieve), standard probe sets ----------------------
+// The first three probes (11, 13, 17) are not probed per window: only the
+// residue classes of q mod 2431 that all three leave alive are visited at all
+// (3 * 9 * 5 = 135 of 2431 for a canonical row), as 32-bit windows of stride 2431
+// (bit i = q0 + 2431 i), and their first kills are counted analytically. The
+// other five register probes (19..37) read strided window tables.
+constexpr uint32_t kWheelM = 2431;                 // 11 * 13 * 17
+constexpr uint32_t kWheelChunk = 32 * kWheelM;     // q covered by one window of every class
+constexpr uint32_t kWheelDivMul = 1766750;         // floor(x / 2431) = umulhi(x, .) for x < 2^20
+constexpr uint32_t kWheelE143 = 1717, kWheelE17 = 715;  // CRT idempotents mod 2431 of (143, 17)
+constexpr int kWheelFirst = 3;                     // register probes 0..2 are the wheel
+constexpr int kWheelReg = 8;                       // register probes of the standard sets (11..37)
+constexpr uint32_t kWheelMidMax = 37681;           // factors below: path "mid" (2 f^2 < 2^32 and f <= 31 M / 2)
+// layout of the wheel tables (32-bit words; k_wheeltab builds, every CTA copies to shared memory)
+constexpr uint32_t kWtKill = 0;      // [3][32] kill masks (bit b = u_r(a, b)) of the rows of 11, 13, 17
+constexpr uint32_t kWtB11 = 96;      // [11][11] entry (a, d): residues t mod 11 with (d t mod 11) alive in row a
+constexpr uint32_t kWtRep11 = 224;   // [11][11][5] entry (a, d): B11(a, d) repeated with period 11 over 143 bits
+constexpr uint32_t kWtRep13 = 832;   // [13][13][5] likewise for 13 (bits >= 143 zero in both)
+constexpr uint32_t kWtNinv143 = 1680;  // [143] x -> (-x^-1) mod 143 (0 where gcd > 1)
+constexpr uint32_t kWtNinv17 = 1824;   // [17]  x -> (-x^-1) mod 17
+constexpr uint32_t kWtTinyOff = 1856;  // [32] f -> word offset of the tiny-factor masks of f (f < 32 prime, not 11, 13, 17)
+constexpr uint32_t kWtTiny = 1888;     // masks (f, t), t < 2f: bits i with f | t + 2431 i   (234 words)
+constexpr uint32_t kWtTab = 2144;    // strided window tables of 19..37: entry (j, a, b), b < 2r:
+                                     // bit i = u_r(a, (b + 2431 i) mod r)
+__host__ __device__ constexpr uint32_t wheel_tab_base(int j)  // first entry of register probe j >= kWheelFirst
+{
+	return j <= kWheelFirst ? kWtTab : wheel_tab_base(j - 1) + 2 * std_prime(j - 1) * std_prime(j - 1);
+}
+constexpr uint32_t kWtWords = wheel_tab_base(kWheelReg);
+constexpr int kWheelQueue = 64;      // per-warp queue of single q alive after the register probes
+constexpr uint32_t kWheelCls = 2432; // per-warp list of alive classes (uint16 offsets below 2431)
+constexpr uint32_t kDefaultRowCostWheel = 5000;  // window-equivalents per row setup for k_wsieve
+constexpr float kDefaultDrainAlphaWheel = 30.0f; // window-equivalents per q queued for the deep probes
+
 struct SieveArgs {
 	const uint32_t* ext;          // row-extended tables
 	uint64_t ext_words;           // (debug bounds checks)
@@ -172,11 +206,18 @@ struct SieveArgs {
 	// slot) and the launch's results are incomplete -- the caller discards
 	// them and re-sieves exactly up to the reference's next stop point
 	const volatile uint32_t* stop;
+	// wheel sieve (k_wsieve): 0 = k_sieve; tables from k_wheeltab
+	uint32_t wheel;
+	const uint32_t* wheeltab;          // [kWtWords]
 };
 
 cudaError_t launch_plan(const SieveArgs& a, cudaStream_t s);
 cudaError_t launch_sieve(const SieveArgs& a, int grid, cudaStream_t s);
 int sieve_grid(int device, int nr2, int nr3, bool std_primes, size_t smem_bytes);
+int wsieve_grid(int device, size_t smem_bytes);
+__host__ __device__ size_t wsieve_smem_bytes(uint32_t np);
+// wheel tables from the row-extended layout; reg_base[j] = ext word offset of register probe j
+cudaError_t launch_wheeltab(const uint32_t* d_ext, const uint32_t* reg_base, uint32_t* d_out, cudaStream_t s);
 __host__ __device__ size_t sieve_smem_bytes(uint32_t np, uint32_t tab_stride);
 __host__ __device__ inline uint32_t plan_chunks(uint32_t n_slots) { return (n_slots + kPlanChunk - 1) / kPlanChunk; }
 

@@ -273,10 +273,16 @@ __device__ __forceinline__ uint32_t factorise_chunk(const SieveArgs& a, PlanSmem
 	// not divide p, times the row's coprime candidates per window
 	float surv = 1.0f, cop = even ? 0.5f : 1.0f;
 	const uint32_t p32 = static_cast<uint32_t>(rb.p);
-	for (uint32_t j = 0; j < a.nreg; ++j)
+	float classes = 1.0f;  // wheel sieve: alive classes of the row relative to a row no wheel prime divides
+	for (uint32_t j = 0; j < a.nreg; ++j) {
 		if (mod_full(p32, a.reg_r[j], a.reg_m[j])) surv *= 1.0f - sm.kill[j];
+		else if (j < static_cast<uint32_t>(kWheelFirst)) classes *= __frcp_rn(fmaxf(1.0f - sm.kill[j], 0.05f));
+	}
 	for (uint32_t j = 0; j < nf; ++j) cop -= cop * __frcp_rn(static_cast<float>(out[1 + j]));
-	const float wt = 1.0f + a.drain_alpha * (1.0f - __expf(-32.0f * cop * surv));
+	// k_wsieve: the loop visits only the alive classes (their share scales the window cost) and
+	// queues single q (32 cop surv per 32-q window), alpha window-equivalents each
+	const float wt = a.wheel ? classes + a.drain_alpha * 32.0f * cop * surv
+	                         : 1.0f + a.drain_alpha * (1.0f - __expf(-32.0f * cop * surv));
 	const uint32_t shift = wt >= 6.0f ? 3u : wt >= 3.0f ? 2u : wt >= 1.5f ? 1u : 0u;
 	out[0] |= shift << 16;
 	return shift;
@@ -820,6 +826,562 @@ __global__ void __launch_bounds__(kSieveThreads, kSieveMinBlocks) k_sieve(const 
 	}
 }
 
+// ---------------------------------------------------------------------------
+// K2w: the wheel sieve (standard probe sets: register probes 11..37).
+//
+// Same contract and row/segment bookkeeping as k_sieve, different window
+// geometry. Probes 11, 13 and 17 are not probed per window at all: a row p
+// leaves alive only the classes of q mod 2431 in A11(p mod 11) x A13(p mod 13)
+// x A17(p mod 17) (135 of 2431 for canonical rows), listed once per row segment,
+// and only those are visited -- as 32-bit windows of STRIDE 2431 (bit i of the
+// window at q0 is q0 + 2431 i, all in one class). The remaining register probes
+// 19..37 read strided window tables (entry (a, q0 mod r) = the 32 kill bits at
+// stride 2431; rows doubled to 2r entries so the lazy Barrett remainder indexes
+// them directly), coprimality is one stride-2431 periodic mask per odd prime
+// factor of p other than 11, 13, 17 (those drop whole classes), and the
+// first-kill counts of 11, 13, 17 come from S0 (candidates), S1 (alive after
+// 11) and S2 (alive after 11 and 13), all by inclusion-exclusion over the
+// factors of p (wheel_counts); S3 on is the telescoped popcount of k_sieve.
+// Lanes still alive after 37 push their single q to the warp queue; the deep
+// probes then run one q per lane.
+// ---------------------------------------------------------------------------
+
+struct WheelSmem {
+	uint32_t* queue;  // [kWheelQueue] q alive after the register probes
+	uint32_t* hist;   // [np]
+	uint4* deep;      // [kDeepPrefetch] {row base, r, m, -}
+	uint16_t* cls;    // [kWheelCls] alive classes: offsets o < 2431 (q = qa + o + 2431 i)
+	uint4* fac;       // [kMaxFactors] loop factors {f, barrett m, x, kind}: kind 0 tiny (x = shared address
+	                  // of its masks), 1 mid (x = -(2431^-1) mod f), 2 large
+	const uint32_t* tab;  // the CTA's wheel tables
+	uint32_t tab0;        // ... as a shared address
+};
+
+// low z bits set, z clamped to [0, 32]
+__device__ __forceinline__ uint32_t low_bits(int z)
+{
+	return ~shl_clamp(kFull, static_cast<uint32_t>(max(0, min(z, 32))));
+}
+
+// #{rho < y : P(rho)} for the 143-bit pattern P, y <= 143
+__device__ __forceinline__ uint32_t prefix143(const uint32_t (&P)[5], uint32_t y)
+{
+	uint32_t c = 0;
+#pragma unroll
+	for (int wd = 0; wd < 5; ++wd) c += __popc(P[wd] & low_bits(static_cast<int>(y) - 32 * wd));
+	return c;
+}
+
+// Warp-collective: S0 = #{q in [qa, qb] : gcd(q, p) = 1}, S1 = those of them
+// alive after probe 11 (row a11), S2 = those alive after 11 and 13, by
+// inclusion-exclusion over the prime factors of p that can divide a q of the
+// row; lanes split the subsets. For a squarefree divisor d the multiples
+// q = d t, t in [t0, t1], have q mod r = (d mod r)(t mod r): the table entry
+// B(a, d mod r) is the set of t residues that stay alive, Rep its periodic
+// extension over the 143 residues of t mod 143.
+__device__ __forceinline__ void wheel_counts(const RowCtx& rc, const WheelSmem& w, uint32_t lane, uint32_t qa,
+                                             uint32_t qb, uint32_t a11, uint32_t a13, uint32_t& s0, uint32_t& s1,
+                                             uint32_t& s2)
+{
+	const uint32_t F = rc.nf + (rc.even ? 1u : 0u);
+	uint32_t acc0 = 0, acc1 = 0, acc2 = 0;  // exact mod 2^32; the results are < 2^32
+	for (uint32_t sub = lane; sub < (1u << F); sub += 32) {
+		uint64_t d = (rc.even && ((sub >> rc.nf) & 1)) ? 2 : 1;
+		for (uint32_t i = 0; i < rc.nf; ++i)
+			if ((sub >> i) & 1) d *= rc.fac[i];
+		if (d > qb) continue;
+		const uint32_t dd = static_cast<uint32_t>(d);
+		const uint32_t t1 = qb / dd, t0 = (qa - 1) / dd + 1;
+		if (t1 < t0) continue;
+		const uint32_t n = t1 - t0 + 1;
+		const uint32_t d11 = dd % 11, d13 = dd % 13;
+		const uint32_t B = w.tab[kWtB11 + a11 * 11 + d11];
+		const uint32_t full = n / 11, rem = n - 11 * full, s = t0 % 11;
+		const uint32_t c1 = full * __popc(B) + __popc(((B | (B << 11)) >> s) & ((1u << rem) - 1));
+		uint32_t P[5];
+		const uint32_t* r11 = w.tab + kWtRep11 + (a11 * 11 + d11) * 5;
+		const uint32_t* r13 = w.tab + kWtRep13 + (a13 * 13 + d13) * 5;
+#pragma unroll
+		for (int wd = 0; wd < 5; ++wd) P[wd] = r11[wd] & r13[wd];
+		const uint32_t tot = prefix143(P, 143);
+		const uint32_t full2 = n / 143, rem2 = n - 143 * full2, sa = t0 % 143, sb = sa + rem2;  // sb <= 285
+		const uint32_t ca = prefix143(P, sa);
+		const uint32_t cb = sb >= 143 ? tot + prefix143(P, sb - 143) : prefix143(P, sb);
+		const uint32_t c2 = full2 * tot + cb - ca;
+		if (__popc(sub) & 1) {
+			acc0 -= n;
+			acc1 -= c1;
+			acc2 -= c2;
+		} else {
+			acc0 += n;
+			acc1 += c1;
+			acc2 += c2;
+		}
+	}
+	s0 = warp_sum(acc0);
+	s1 = warp_sum(acc1);
+	s2 = warp_sum(acc2);
+}
+
+// Deep probes for queue entries [base, base + n), one q per lane, in rank
+// order; the lanes leave together once every q is dead. Survivors are emitted.
+__device__ __forceinline__ void wheel_drain(const SieveArgs& a, const WheelSmem& w, uint32_t lane, uint32_t base,
+                                            uint32_t n, uint32_t p, uint32_t& kmax)
+{
+	bool alive = lane < n;
+	const uint32_t q = alive ? w.queue[base + lane] : 0u;
+	for (uint32_t j = kWheelReg; j < a.np; ++j) {
+		if (!__any_sync(kFull, alive)) break;
+		bool kill = false;
+		if (alive) {
+			uint32_t row, r, m;
+			if (j - kWheelReg < kDeepPrefetch) {
+				const uint4 e = w.deep[j - kWheelReg];
+				row = e.x;
+				r = e.y;
+				m = e.z;
+			} else {
+				const uint4 d = __ldg(a.probes + j);
+				row = d.z + mod_full(p, d.x, d.y) * d.w;
+				r = d.x;
+				m = d.y;
+			}
+			const uint32_t b = mod_full(q, r, m);
+			CGPU_CHECK(row + (b >> 5) < a.ext_words);
+			kill = (__ldg(a.ext + row + (b >> 5)) >> (b & 31)) & 1u;
+		}
+		const uint32_t km = __ballot_sync(kFull, kill);
+		if (km) {
+			kmax = max(kmax, j + 1);
+			if (lane == 0) hist_add(a, w.hist, j, __popc(km));
+			alive = alive && !kill;
+		}
+	}
+	const uint32_t sm = __ballot_sync(kFull, alive);
+	if (sm) {
+		unsigned long long sb = 0;
+		if (lane == 0) sb = atomicAdd(&a.counters[1], static_cast<unsigned long long>(__popc(sm)));
+		sb = __shfl_sync(kFull, sb, 0) + __popc(sm & ((1u << lane) - 1));
+		if (alive && sb < a.surv_cap) a.surv[sb] = (static_cast<unsigned long long>(p) << 32) | q;
+	}
+}
+
+// One row segment: q in [rc.qlo + 32 rc.w0, min(rc.qhi, rc.qlo + 32 rc.w1 - 1)].
+// nfl = the loop's factor slots in w.fac (odd prime factors of p other than
+// 11, 13, 17). Returns 1 + the deepest probe that killed in the segment (0: none).
+__device__ __forceinline__ uint32_t wheel_row(const SieveArgs& a, const WheelSmem& w, uint32_t lane,
+                                              const RowCtx& rc, uint32_t nfl)
+{
+	const uint32_t qa = rc.qlo + 32 * rc.w0;
+	const uint64_t qe = uint64_t(rc.qlo) + 32ull * rc.w1 - 1;  // 64-bit: no 2^32 wrap
+	const uint32_t qb = qe < rc.qhi ? static_cast<uint32_t>(qe) : rc.qhi;
+	const uint32_t span = qb - qa;
+	const uint32_t lt = (1u << lane) - 1;
+	uint32_t kmax = 0;
+
+	// rows of the wheel primes; a class killed by one of them is dropped, and when
+	// the prime divides p its class 0 holds no coprime q at all
+	const uint32_t a11 = mod_full(rc.p, 11, barrett_m(11)), a13 = mod_full(rc.p, 13, barrett_m(13));
+	const uint32_t a17 = mod_full(rc.p, 17, barrett_m(17));
+	const uint32_t kill11 = w.tab[kWtKill + a11] | (a11 ? 0u : 1u);
+	const uint32_t kill13 = w.tab[kWtKill + 32 + a13] | (a13 ? 0u : 1u);
+	const uint32_t kill17 = w.tab[kWtKill + 64 + a17] | (a17 ? 0u : 1u);
+	const uint32_t qa11 = mod_full(qa, 11, barrett_m(11)), qa13 = mod_full(qa, 13, barrett_m(13));
+	const uint32_t qa17 = mod_full(qa, 17, barrett_m(17));
+	// the segment's alive offsets mod 143 (cls[0 .. n143)) and mod 17 (cls[160 .. 160 + n17)), then
+	// their CRT combinations o < 2431 with o <= span, written over the list from the top down so
+	// that the two inputs (read in ascending order of ci / n17) are consumed before being overwritten
+	uint32_t n143 = 0;
+#pragma unroll
+	for (uint32_t c0 = 0; c0 < 143; c0 += 32) {
+		const uint32_t c = c0 + lane;
+		const uint32_t x11 = mod_full(qa11 + c, 11, barrett_m(11)), x13 = mod_full(qa13 + c, 13, barrett_m(13));
+		const bool ok = c < 143 && !((kill11 >> x11) & 1u) && !((kill13 >> x13) & 1u);
+		const uint32_t bal = __ballot_sync(kFull, ok);
+		if (ok) w.cls[kWheelCls - 192 + n143 + __popc(bal & lt)] = static_cast<uint16_t>(c);
+		n143 += __popc(bal);
+	}
+	uint32_t n17;
+	{
+		const uint32_t x17 = mod_full(qa17 + lane, 17, barrett_m(17));
+		const bool ok = lane < 17 && !((kill17 >> x17) & 1u);
+		const uint32_t bal = __ballot_sync(kFull, ok);
+		if (ok) w.cls[kWheelCls - 32 + __popc(bal & lt)] = static_cast<uint16_t>(lane);
+		n17 = __popc(bal);
+	}
+	__syncwarp();
+	uint32_t n = 0;
+	{
+		// The staging lists sit in the top 192 entries of cls; a full product (143 x 17 = 2431 > 2240)
+		// would overwrite them, so they are first copied to registers: lane l holds L143[l + 32 m]
+		// (m < 5) and L17[l] and the combinations are formed with shuffles.
+		uint32_t l143[5], l17;
+#pragma unroll
+		for (int m = 0; m < 5; ++m) l143[m] = (32 * m + lane < n143) ? w.cls[kWheelCls - 192 + 32 * m + lane] : 0u;
+		l17 = lane < n17 ? w.cls[kWheelCls - 32 + lane] : 0u;
+		__syncwarp();
+		const uint32_t ntot = n143 * n17;
+		const uint32_t rcp17 = 65536u / max(n17, 1u) + 1;  // floor(ci / n17) = (ci * rcp17) >> 16 for ci < 2432
+		for (uint32_t c0 = 0; c0 < ntot; c0 += 32) {
+			const uint32_t ci = c0 + lane;
+			const uint32_t i143 = (ci * rcp17) >> 16, i17 = ci - i143 * n17;
+			uint32_t o143 = 0;
+#pragma unroll
+			for (int m = 0; m < 5; ++m) {
+				const uint32_t v = __shfl_sync(kFull, l143[m], i143 & 31);
+				if ((i143 >> 5) == static_cast<uint32_t>(m)) o143 = v;
+			}
+			const uint32_t o17 = __shfl_sync(kFull, l17, i17 & 31);
+			const uint32_t o = mod_full(o143 * kWheelE143 + o17 * kWheelE17, kWheelM, barrett_m(kWheelM));
+			const bool ok = ci < ntot && o <= span;
+			const uint32_t bal = __ballot_sync(kFull, ok);
+			if (ok) w.cls[n + __popc(bal & lt)] = static_cast<uint16_t>(o);
+			n += __popc(bal);
+		}
+	}
+	__syncwarp();
+
+	// S[j - kWheelFirst] = sum of popc(alive before register probe j), j = 3..7
+	uint32_t S[kWheelReg - kWheelFirst];
+#pragma unroll
+	for (int j = 0; j < kWheelReg - kWheelFirst; ++j) S[j] = 0;
+	uint32_t entered = 0, qn = 0;
+
+	if (n) {
+		// shared address of row (p mod r) of each strided window table
+		uint32_t ta[kWheelReg - kWheelFirst];
+#pragma unroll
+		for (int j = kWheelFirst; j < kWheelReg; ++j) {
+			const uint32_t r = std_prime(j);
+			ta[j - kWheelFirst] = w.tab0 + 4 * (wheel_tab_base(j) + mod_full(rc.p, r, barrett_m(r)) * 2 * r);
+		}
+		const uint32_t evenm = rc.even ? 0x55555555u : 0u;  // q0 + 2431 i alternates parity
+		const uint32_t nchunk = span / kWheelChunk + 1;
+		const uint32_t total = n * nchunk;
+		const uint32_t n_iter = (total + 31) / 32;
+		const uint32_t kfull = (span + 1) / kWheelChunk;  // chunks lying wholly inside the segment
+		const uint32_t n_full = (n * kfull) / 32;
+		uint32_t k = lane / n, ci = lane - k * n;
+		const uint32_t dk = 32 / n, dc = 32 - dk * n;
+
+		for (uint32_t it = 0;; ++it) {
+			const bool last = it >= n_iter;  // one more pass to drain what is left in the queue
+			uint32_t alive = 0, q0 = 0;
+			if (!last) {
+				const uint32_t c = w.cls[ci];
+				q0 = qa + c + kWheelChunk * k;
+				uint32_t nonc = evenm << (q0 & 1u);
+				for (uint32_t s = 0; s < nfl; ++s) {  // warp-uniform paths
+					const uint4 e = w.fac[s];
+					uint32_t t = mod_lazy(q0, e.x, e.y);
+					if (e.w == 0) {  // f < 32: masks of (f, t), t < 2f, in shared memory
+						uint32_t mk;
+						asm volatile("ld.shared.u32 %0, [%1];" : "=r"(mk) : "r"(e.z + 4 * t));
+						nonc |= mk;
+					} else if (e.w == 1) {  // first i with f | q0 + 2431 i is t g mod f; at most one below 32
+						nonc |= shl_clamp(1u, mod_full(t * e.z, e.x, e.y));
+					} else {  // f >= 37681: at most two multiples of f in [q0, q0 + 31 * 2431]
+						t = min(t, t - e.x);
+						uint32_t d = t ? e.x - t : 0u;
+#pragma unroll
+						for (int rep = 0; rep < 2; ++rep) {
+							const uint32_t i = __umulhi(min(d, kWheelChunk), kWheelDivMul);
+							nonc |= i * kWheelM == d ? shl_clamp(1u, i) : 0u;
+							d += e.x;  // < 2^32: f < 2^32 / 59 ... f <= p < 2^32 in TRIANGLE -> clamp below
+							if (d < e.x) d = kWheelChunk + 1;  // wrapped: no further multiple in reach
+						}
+					}
+				}
+				alive = ~nonc;
+				if (it >= n_full) {  // edge: the row's last chunks and lanes past the end
+					uint32_t vm = 0;
+					if (k < nchunk) {
+						const uint32_t rem = span - kWheelChunk * k;
+						if (c <= rem) vm = ~shl_clamp(kFull, __umulhi(min(rem - c, kWheelChunk - 1), kWheelDivMul) + 1);
+					}
+					alive &= vm;
+				}
+				S[0] += __popc(alive);
+#pragma unroll
+				for (int j = kWheelFirst; j < kWheelReg; ++j) {
+					const uint32_t r = std_prime(j);
+					const uint32_t rem = mod_lazy(q0, r, barrett_m(r));  // [0, 2r): the rows are doubled
+					uint32_t M;
+					asm volatile("ld.shared.u32 %0, [%1];" : "=r"(M) : "r"(ta[j - kWheelFirst] + 4 * rem));
+					alive &= ~M;
+					if (j + 1 < kWheelReg) S[j + 1 - kWheelFirst] += __popc(alive);
+				}
+				ci += dc;
+				k += dk;
+				if (ci >= n) {
+					ci -= n;
+					++k;
+				}
+			}
+			uint32_t m = __ballot_sync(kFull, alive != 0);
+			do {
+				if (m) {
+					CGPU_CHECK(qn + __popc(m) <= kWheelQueue);
+					if (alive) {
+						const uint32_t bit = __ffs(alive) - 1;
+						w.queue[qn + __popc(m & lt)] = q0 + kWheelM * bit;
+						alive &= alive - 1;
+					}
+					qn += __popc(m);
+				}
+				if (qn >= 32 || (last && qn)) {
+					const uint32_t nd = min(qn, 32u);
+					__syncwarp();
+					qn -= nd;
+					entered += nd;
+					wheel_drain(a, w, lane, qn, nd, rc.p, kmax);
+					__syncwarp();
+				}
+				m = __ballot_sync(kFull, alive != 0);
+			} while (m);
+			if (last) break;
+		}
+	}
+	// first-kill counts of the register probes
+	uint32_t tot[kWheelReg + 1];
+	wheel_counts(rc, w, lane, qa, qb, a11, a13, tot[0], tot[1], tot[2]);
+#pragma unroll
+	for (int j = kWheelFirst; j < kWheelReg; ++j) tot[j] = warp_sum(S[j - kWheelFirst]);
+	tot[kWheelReg] = entered;
+#pragma unroll
+	for (int j = 0; j < kWheelReg; ++j) {
+		const uint32_t s = tot[j] - tot[j + 1];
+		if (s) {
+			kmax = max(kmax, static_cast<uint32_t>(j + 1));
+			if (lane == 0) hist_add(a, w.hist, j, s);
+		}
+	}
+	return kmax;
+}
+
+template <bool STOP>
+__global__ void __launch_bounds__(kSieveThreads, 1) k_wsieve(const SieveArgs a)
+{
+	extern __shared__ uint4 s_dyn[];
+	__shared__ bool s_last;
+	__shared__ unsigned long long s_red[kSieveWarps];
+	const uint32_t lane = threadIdx.x & 31;
+	const uint32_t wib = threadIdx.x >> 5;
+	WheelSmem w;
+	uint4* deep_all = s_dyn;
+	uint4* fac_all = deep_all + kSieveWarps * kDeepPrefetch;
+	uint32_t* q_all = reinterpret_cast<uint32_t*>(fac_all + kSieveWarps * kMaxFactors);
+	uint16_t* cls_all = reinterpret_cast<uint16_t*>(q_all + kSieveWarps * kWheelQueue);
+	uint32_t* s_tab = reinterpret_cast<uint32_t*>(cls_all + kSieveWarps * kWheelCls);
+	uint32_t* h_all = s_tab + kWtWords;
+	w.deep = deep_all + wib * kDeepPrefetch;
+	w.fac = fac_all + wib * kMaxFactors;
+	w.queue = q_all + wib * kWheelQueue;
+	w.cls = cls_all + wib * kWheelCls;
+	w.hist = h_all + static_cast<size_t>(wib) * a.np;
+	w.tab = s_tab;
+	w.tab0 = static_cast<uint32_t>(__cvta_generic_to_shared(s_tab));
+	for (uint32_t j = lane; j < a.np; j += 32) w.hist[j] = 0;
+	for (uint32_t e = threadIdx.x; e < kWtWords; e += blockDim.x) s_tab[e] = __ldg(a.wheeltab + e);
+	__syncthreads();
+	CGPU_CHECK(wsieve_smem_bytes(a.np) <= dynamic_smem_size());
+
+	const uint32_t n_chunks = plan_chunks(a.n_slots);
+	const unsigned long long W = a.chunk_off[n_chunks];
+	const unsigned long long nwarps = static_cast<unsigned long long>(gridDim.x) * kSieveWarps;
+	const unsigned long long gw = static_cast<unsigned long long>(blockIdx.x) * kSieveWarps + wib;
+	unsigned long long ws = W * gw / nwarps;  // W < 2^40, nwarps < 2^20
+	const unsigned long long we = W * (gw + 1) / nwarps;
+
+	// 32-ary warp search: largest slot s with prefix(s) <= ws
+	uint32_t lo = 0, hi = a.n_slots;
+	if (ws < we) {
+		while (hi - lo > 1) {
+			const uint32_t step = (hi - lo + 31) / 32;
+			const uint32_t idx = lo + step * lane;
+			const bool le = idx < hi && slot_prefix(a, idx) <= ws;
+			const uint32_t L = 31 - __clz(__ballot_sync(kFull, le));
+			lo += step * L;
+			hi = min(hi, lo + step);
+		}
+	}
+
+	uint32_t slot = lo;
+	while (ws < we) {
+		const unsigned long long rs = slot_prefix(a, slot), re = slot_prefix(a, slot + 1);
+		if (re <= ws) {
+			++slot;
+			continue;
+		}
+		const unsigned long long u0 = ws - rs, u1 = min(we, re) - rs;
+		ws = min(we, re);
+		const uint32_t cur = slot++;
+		if constexpr (STOP)  // a stop raised: abandon the launch (the caller re-sieves exactly)
+			if (a.stop && (cur & 7u) == 0 && *a.stop) break;
+		if (u1 <= a.row_cost) continue;
+		const RowBounds rb = slot_row(a, cur);
+		RowCtx rc;
+		rc.p = static_cast<uint32_t>(rb.p);
+		rc.qlo = static_cast<uint32_t>(rb.qlo);
+		rc.qhi = static_cast<uint32_t>(rb.qhi);
+		rc.wlast = (rc.qhi - rc.qlo) / 32;
+		rc.tail = 0;
+		const uint32_t fw = lane < kFacWords ? __ldg(a.rowfac + static_cast<size_t>(cur) * kFacWords + lane) : 0u;
+		const uint32_t head = __shfl_sync(kFull, fw, 0);
+		rc.nf = head & 0xffu;
+		rc.even = (head >> 8) & 1u;
+		rc.w0 = unit_window(a, u0, (head >> 16) & 3u, rc.wlast + 1);
+		rc.w1 = unit_window(a, u1, (head >> 16) & 3u, rc.wlast + 1);
+		if (rc.w1 <= rc.w0) continue;
+#pragma unroll
+		for (int k = 0; k < kMaxFactors; ++k) {
+			rc.fac[k] = __shfl_sync(kFull, fw, k + 1);
+			rc.fm[k] = __shfl_sync(kFull, fw, k + 1 + kMaxFactors);
+		}
+		// the loop's factor slots: odd factors other than 11, 13, 17 (lane L = 1..nf holds factor L - 1)
+		const uint32_t fmv = __shfl_down_sync(kFull, fw, kMaxFactors);  // lane L: its Barrett constant
+		const bool keep = lane >= 1 && lane <= rc.nf && fw != 11 && fw != 13 && fw != 17;
+		const uint32_t keepm = __ballot_sync(kFull, keep);
+		if (keep) {
+			uint32_t x = 0, kind = 2;
+			if (fw < 32) {  // tiny: masks in shared memory
+				kind = 0;
+				x = w.tab0 + 4 * w.tab[kWtTinyOff + fw];
+			} else if (fw < kWheelMidMax) {
+				// g = -(2431^-1) mod f; 143^-1 = (1 + f k) / 143 with k = (-f^-1) mod 143, likewise 17^-1
+				kind = 1;
+				const uint32_t i143 = (1 + fw * w.tab[kWtNinv143 + fw % 143]) / 143;
+				const uint32_t i17 = (1 + fw * w.tab[kWtNinv17 + fw % 17]) / 17;
+				x = fw - mod_full(i143 * i17, fw, fmv);
+			}
+			w.fac[__popc(keepm & ((1u << lane) - 1))] = make_uint4(fw, fmv, x, kind);
+		}
+		const uint32_t nfl = __popc(keepm);
+		// rows of the first deep probes, pulled into L1
+		if (kWheelReg + lane / 2 < a.np && lane < 2 * kDeepPrefetch) {
+			const uint4 d = __ldg(a.probes + kWheelReg + lane / 2);
+			const uint32_t base = d.z + mod_full(rc.p, d.x, d.y) * d.w;
+			if ((lane & 1) == 0) w.deep[lane / 2] = make_uint4(base, d.x, d.y, 0);
+			const uint32_t* row = a.ext + base + (lane & 1) * 32;
+			if ((lane & 1) == 0 || d.w > 32) asm volatile("prefetch.global.L1 [%0];" ::"l"(row));
+		}
+		__syncwarp();
+
+		const uint32_t kk = wheel_row(a, w, lane, rc, nfl);
+		if (lane == 0 && kk) {
+			const uint32_t j = kk - 1;
+			const uint32_t killer = j < static_cast<uint32_t>(kWheelReg) ? std_prime(j) : __ldg(a.probes + j).x;
+			CGPU_CHECK(rb.p / 100 - a.blk_lo < a.n_blocks);
+			atomicMax(&a.block_rmax[rb.p / 100 - a.blk_lo], killer);
+		}
+		__syncwarp();
+	}
+
+	// ---- CTA flush: per-warp counters -> global histogram ----
+	__syncthreads();
+	for (uint32_t j = threadIdx.x; j < a.np; j += blockDim.x) {
+		unsigned long long s = 0;
+		for (int v = 0; v < kSieveWarps; ++v) s += h_all[static_cast<size_t>(v) * a.np + j];
+		if (s) atomicAdd(&a.hist[__ldg(a.probe_rank + j)], s);
+	}
+	__threadfence();
+	__syncthreads();
+	if (threadIdx.x == 0) s_last = atomicAdd(&a.tickets[1], 1u) == gridDim.x - 1;
+	__syncthreads();
+	if (!s_last) return;
+	__threadfence();
+	unsigned long long s = 0;
+	for (uint32_t k = threadIdx.x; k < a.nprimes; k += blockDim.x)
+		s += *reinterpret_cast<volatile unsigned long long*>(a.hist + k);
+	for (int d = 16; d; d >>= 1) s += __shfl_xor_sync(kFull, s, d);
+	if (lane == 0) s_red[wib] = s;
+	__syncthreads();
+	if (threadIdx.x == 0) {
+		unsigned long long t = 0;
+		for (int v = 0; v < kSieveWarps; ++v) t += s_red[v];
+		a.counters[0] = t + *reinterpret_cast<volatile unsigned long long*>(a.counters + 1);
+		a.tickets[1] = 0;
+	}
+}
+
+// Wheel tables from the row-extended layout (kernels.cuh kWt*): one thread per word.
+struct WheelTabArgs {
+	uint32_t base[kWheelReg];  // ext word offset of register probe j's rows
+};
+
+__global__ void k_wheeltab(const uint32_t* __restrict__ ext, const WheelTabArgs t, uint32_t* __restrict__ out)
+{
+	auto ubit = [&](int j, uint32_t a, uint32_t x) -> uint32_t {  // u_r(a, x), x < r
+		const uint32_t r = std_prime(j);
+		return (ext[t.base[j] + a * ext_row_words(r) + (x >> 5)] >> (x & 31)) & 1u;
+	};
+	for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < kWtWords; e += gridDim.x * blockDim.x) {
+		uint32_t v = 0;
+		if (e < kWtB11) {  // kill masks of 11 (words 0..31), 13 (32..63), 17 (64..95)
+			const int j = e >> 5;
+			const uint32_t r = std_prime(j), a = e & 31;
+			if (a < r)
+				for (uint32_t b = 0; b < r; ++b) v |= ubit(j, a, b) << b;
+		} else if (e < kWtRep11) {  // B(a, d): t residues with (d t mod 11) alive in row a of 11
+			const uint32_t i = e - kWtB11;
+			if (i < 121) {
+				const uint32_t a = i / 11, d = i % 11;
+				for (uint32_t rho = 0; rho < 11; ++rho) v |= (ubit(0, a, (d * rho) % 11) ^ 1u) << rho;
+			}
+		} else if (e < kWtNinv143) {  // B(a, d) of 11 / 13 repeated over the 143 residues of t, 5 words
+			const int j = e < kWtRep13 ? 0 : 1;
+			const uint32_t r = std_prime(j), i = e - (j ? kWtRep13 : kWtRep11);
+			if (i < r * r * 5) {
+				const uint32_t a = i / (5 * r), d = (i / 5) % r, wd = i % 5;
+				for (uint32_t l = 0; l < 32; ++l) {
+					const uint32_t rho = 32 * wd + l;
+					if (rho < 143) v |= (ubit(j, a, (d * (rho % r)) % r) ^ 1u) << l;
+				}
+			}
+		} else if (e < kWtNinv17) {  // x -> (-x^-1) mod 143
+			const uint32_t x = e - kWtNinv143;
+			if (x < 143)
+				for (uint32_t y = 1; y < 143; ++y)
+					if ((x * y) % 143 == 142) v = y;
+		} else if (e < kWtTinyOff) {  // x -> (-x^-1) mod 17
+			const uint32_t x = e - kWtNinv17;
+			if (x < 17)
+				for (uint32_t y = 1; y < 17; ++y)
+					if ((x * y) % 17 == 16) v = y;
+		} else if (e < kWtTab) {  // tiny-factor masks: offsets by f, then (f, t), t < 2f: bits i with f | t + 2431 i
+			uint32_t off = kWtTiny;
+			bool done = false;
+			for (uint32_t f = 3; f < 32 && !done; f += 2) {
+				bool prime = true;
+				for (uint32_t dv = 3; dv * dv <= f; dv += 2) prime = prime && (f % dv != 0);
+				if (!prime || f == 11 || f == 13 || f == 17) continue;
+				if (e == kWtTinyOff + f) {
+					v = off;
+					done = true;
+				} else if (e >= off && e < off + 2 * f) {
+					const uint32_t t = e - off;
+					for (uint32_t l = 0; l < 32; ++l)
+						if ((t + kWheelM * l) % f == 0) v |= 1u << l;
+					done = true;
+				}
+				off += 2 * f;
+			}
+		} else {
+			int j = kWheelFirst;
+			while (j + 1 < kWheelReg && e >= wheel_tab_base(j + 1)) ++j;
+			const uint32_t r = std_prime(j), i = e - wheel_tab_base(j), a = i / (2 * r), b = i % (2 * r);
+			for (uint32_t l = 0; l < 32; ++l) v |= ubit(j, a, (b + kWheelM * l) % r) << l;
+		}
+		out[e] = v;
+	}
+}
+
+template <bool STOP>
+void* wsieve_fn()
+{
+	return reinterpret_cast<void*>(&k_wsieve<STOP>);
+}
+
 // block r_max init: 1 for blocks owned by this shard, 0 otherwise
 __global__ void k_init_blocks(uint32_t* rmax, uint64_t n, uint64_t blk_lo, uint32_t G, uint32_t g)
 {
@@ -920,6 +1482,37 @@ int sieve_grid(int device, int nr2, int nr3, bool std_primes, size_t smem)
 	return sms * per_sm;
 }
 
+__host__ __device__ size_t wsieve_smem_bytes(uint32_t np)
+{
+	return sizeof(uint4) * kSieveWarps * (kDeepPrefetch + kMaxFactors) + sizeof(uint32_t) * kSieveWarps * kWheelQueue +
+	       sizeof(uint16_t) * kSieveWarps * kWheelCls + sizeof(uint32_t) * kWtWords +
+	       sizeof(uint32_t) * static_cast<size_t>(np) * kSieveWarps;
+}
+
+int wsieve_grid(int device, size_t smem)
+{
+	int sms = 0, per_sm = 0, optin = 0;
+	cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+	cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+	const void* variants[2] = {wsieve_fn<true>(), wsieve_fn<false>()};
+	for (const void* f : variants) {
+		cudaFuncAttributes fa{};
+		cudaFuncGetAttributes(&fa, f);
+		cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - static_cast<int>(fa.sharedSizeBytes));
+	}
+	cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, variants[0], kSieveThreads, smem);
+	if (per_sm < 1) per_sm = 1;
+	return sms * per_sm;
+}
+
+cudaError_t launch_wheeltab(const uint32_t* d_ext, const uint32_t* reg_base, uint32_t* d_out, cudaStream_t s)
+{
+	WheelTabArgs t;
+	for (int j = 0; j < kWheelReg; ++j) t.base[j] = reg_base[j];
+	k_wheeltab<<<(kWtWords + 127) / 128, 128, 0, s>>>(d_ext, t, d_out);
+	return cudaGetLastError();
+}
+
 cudaError_t launch_plan(const SieveArgs& a, cudaStream_t s)
 {
 	k_plan<<<plan_chunks(a.n_slots), kPlanChunk, 0, s>>>(a);
@@ -930,6 +1523,9 @@ cudaError_t launch_sieve(const SieveArgs& a, int grid, cudaStream_t s)
 {
 	const size_t smem = sieve_smem_bytes(a.np, a.wtab_n ? (a.std_primes ? kTabStrideStd : kTabStrideGen) : 0);
 	void* args[] = {const_cast<SieveArgs*>(&a)};
+	if (a.wheel)
+		return cudaLaunchKernel(a.stop != nullptr ? wsieve_fn<true>() : wsieve_fn<false>(), dim3(grid),
+		                        dim3(kSieveThreads), args, wsieve_smem_bytes(a.np), s);
 	return cudaLaunchKernel(sieve_kernel_ptr(static_cast<int>(a.nreg2), static_cast<int>(a.nreg3), a.std_primes,
 	                                         a.stop != nullptr, a.short_rows != 0),
 	                        dim3(grid),
