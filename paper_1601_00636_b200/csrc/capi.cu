@@ -169,7 +169,7 @@ struct cgpu_ctx {
 	DevBuf<uint32_t> wheeltab;
 	int wgrid = 0;
 	uint32_t row_cost_wheel = kDefaultRowCostWheel;
-	float drain_alpha_wheel = kDefaultDrainAlphaWheel;
+	float wheel_cost[4] = {kDefaultWheelCost[0], kDefaultWheelCost[1], kDefaultWheelCost[2], kDefaultWheelCost[3]};
 	int grid = 0;
 	std::map<uint64_t, int> grid_cache;
 
@@ -254,7 +254,8 @@ int cgpu_create(int device, void* stream, cgpu_ctx** out)
 	if (const char* da = std::getenv("CUBOID_DRAIN_ALPHA")) c->drain_alpha = static_cast<float>(std::atof(da));
 	if (const char* wh = std::getenv("CUBOID_WHEEL")) c->wheel_enabled = std::atoi(wh) != 0;
 	if (const char* rw = std::getenv("CUBOID_ROW_COST_WHEEL")) c->row_cost_wheel = static_cast<uint32_t>(std::atoi(rw));
-	if (const char* aw = std::getenv("CUBOID_DRAIN_ALPHA_WHEEL")) c->drain_alpha_wheel = static_cast<float>(std::atof(aw));
+	if (const char* wc = std::getenv("CUBOID_WHEEL_COSTS"))  // "base,mid,large,queued" instructions
+		std::sscanf(wc, "%f,%f,%f,%f", &c->wheel_cost[0], &c->wheel_cost[1], &c->wheel_cost[2], &c->wheel_cost[3]);
 	if (const char* sr = std::getenv("CUBOID_SHORT_ROWS")) c->short_rows = std::atoi(sr) < 0 ? -1 : (std::atoi(sr) ? 1 : 0);
 	for (auto& e : c->ev) cudaEventCreate(&e);
 	// trial-division primes below 2^16 (covers sqrt of any p < 2^32)
@@ -986,7 +987,7 @@ int enqueue_sieve(cgpu_ctx* c, uint64_t p_lo, uint64_t q_start, uint64_t p_hi, u
 	a.wheeltab = c->wheeltab.p;
 	if (a.wheel) {
 		a.row_cost = c->row_cost_wheel;
-		a.drain_alpha = c->drain_alpha_wheel;
+		for (int k = 0; k < 4; ++k) a.wheel_cost[k] = c->wheel_cost[k];
 	}
 	a.p_lo = p_lo;
 	a.p_hi = p_hi;

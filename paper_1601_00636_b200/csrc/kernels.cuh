@@ -156,8 +156,10 @@ __host__ __device__ constexpr uint32_t wheel_tab_base(int j)  // first entry of 
 constexpr uint32_t kWtWords = wheel_tab_base(kWheelReg);
 constexpr int kWheelQueue = 64;      // per-warp queue of single q alive after the register probes
 constexpr uint32_t kWheelCls = 2432; // per-warp list of alive classes (uint16 offsets below 2431)
-constexpr uint32_t kDefaultRowCostWheel = 5000;  // window-equivalents per row setup for k_wsieve
-constexpr float kDefaultDrainAlphaWheel = 30.0f; // window-equivalents per q queued for the deep probes
+// k_wsieve's load-balance model (k_plan), in instructions, from the ncu instruction counts of C5:
+// per row segment, then per loop iteration {base, per factor below 37681, per factor above}, per queued q
+constexpr uint32_t kDefaultRowCostWheel = 1800 * 64;  // units of 1/64 instruction
+constexpr float kDefaultWheelCost[4] = {120.0f, 14.0f, 30.0f, 25.0f};
 
 struct SieveArgs {
 	const uint32_t* ext;          // row-extended tables
@@ -209,6 +211,7 @@ struct SieveArgs {
 	// wheel sieve (k_wsieve): 0 = k_sieve; tables from k_wheeltab
 	uint32_t wheel;
 	const uint32_t* wheeltab;          // [kWtWords]
+	float wheel_cost[4];               // load-balance model (kDefaultWheelCost)
 };
 
 cudaError_t launch_plan(const SieveArgs& a, cudaStream_t s);

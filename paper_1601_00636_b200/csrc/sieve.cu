@@ -137,7 +137,20 @@ __device__ __forceinline__ uint64_t row_windows(const RowBounds& b)
 __device__ __forceinline__ uint64_t row_units(const SieveArgs& a, const RowBounds& b, uint32_t shift)
 {
 	const uint64_t w = row_windows(b);
+	// k_wsieve: `shift` is the row's cost per window in units of 1/64 instruction (wheel_mult)
+	if (a.wheel) return w ? a.row_cost + w * shift : 0;
 	return w ? a.row_cost + (w << shift) : 0;
+}
+
+// k_wsieve's inverse of row_units: first window of the row at unit u. Rows that lie wholly in a
+// warp's slice (nearly all) take the shortcuts; only split rows divide.
+__device__ __forceinline__ uint32_t unit_window_mult(const SieveArgs& a, unsigned long long u, uint32_t mult,
+                                                     uint32_t windows)
+{
+	if (u <= a.row_cost) return 0;
+	const unsigned long long x = u - a.row_cost;
+	if (x >= static_cast<unsigned long long>(windows) * mult) return windows;
+	return static_cast<uint32_t>((x + mult - 1) / mult);
 }
 
 // First window of the row at unit u (the inverse of row_units; monotonic, so
@@ -273,16 +286,40 @@ __device__ __forceinline__ uint32_t factorise_chunk(const SieveArgs& a, PlanSmem
 	// not divide p, times the row's coprime candidates per window
 	float surv = 1.0f, cop = even ? 0.5f : 1.0f;
 	const uint32_t p32 = static_cast<uint32_t>(rb.p);
-	float classes = 1.0f;  // wheel sieve: alive classes of the row relative to a row no wheel prime divides
-	for (uint32_t j = 0; j < a.nreg; ++j) {
+	for (uint32_t j = 0; j < a.nreg; ++j)
 		if (mod_full(p32, a.reg_r[j], a.reg_m[j])) surv *= 1.0f - sm.kill[j];
-		else if (j < static_cast<uint32_t>(kWheelFirst)) classes *= __frcp_rn(fmaxf(1.0f - sm.kill[j], 0.05f));
-	}
 	for (uint32_t j = 0; j < nf; ++j) cop -= cop * __frcp_rn(static_cast<float>(out[1 + j]));
-	// k_wsieve: the loop visits only the alive classes (their share scales the window cost) and
-	// queues single q (32 cop surv per 32-q window), alpha window-equivalents each
-	const float wt = a.wheel ? classes + a.drain_alpha * 32.0f * cop * surv
-	                         : 1.0f + a.drain_alpha * (1.0f - __expf(-32.0f * cop * surv));
+	if (a.wheel) {
+		// k_wsieve: instructions of the row's loop = iterations x (base + per factor) + queued q x
+		// drain cost, spread over the row's windows in units of 1/64 instruction (16 bits). The
+		// iterations step with the row length (one more window per class every 77792 q) and with
+		// the alive classes of q mod 2431 (the wheel primes that divide p leave all but class 0).
+		const uint64_t wn = row_windows(rb);
+		uint32_t mult = 1;
+		if (wn) {
+			float classes = 1.0f;
+			for (uint32_t j = 0; j < static_cast<uint32_t>(kWheelFirst); ++j) {
+				const float r = static_cast<float>(a.reg_r[j]);
+				classes *= mod_full(p32, a.reg_r[j], a.reg_m[j]) ? rintf(r * (1.0f - sm.kill[j])) : r - 1.0f;
+			}
+			uint32_t nmid = 0, nlarge = 0;
+			for (uint32_t j = 0; j < nf; ++j) {
+				const uint32_t f = out[1 + j];
+				if (f == a.reg_r[0] || f == a.reg_r[1] || f == a.reg_r[2]) continue;
+				if (f < kWheelMidMax) ++nmid;
+				else ++nlarge;
+			}
+			const float q = static_cast<float>(wn) * 32.0f;
+			const float nchunk = floorf((q - 1.0f) * (1.0f / kWheelChunk)) + 1.0f;
+			const float iters = ceilf(classes * nchunk * (1.0f / 32.0f)) + 1.0f;
+			const float cost = iters * (a.wheel_cost[0] + a.wheel_cost[1] * nmid + a.wheel_cost[2] * nlarge) +
+			                   q * cop * surv * a.wheel_cost[3];
+			mult = static_cast<uint32_t>(fminf(fmaxf(rintf(64.0f * cost / static_cast<float>(wn)), 1.0f), 65535.0f));
+		}
+		out[0] |= mult << 16;
+		return mult;
+	}
+	const float wt = 1.0f + a.drain_alpha * (1.0f - __expf(-32.0f * cop * surv));
 	const uint32_t shift = wt >= 6.0f ? 3u : wt >= 3.0f ? 2u : wt >= 1.5f ? 1u : 0u;
 	out[0] |= shift << 16;
 	return shift;
@@ -851,8 +888,7 @@ struct WheelSmem {
 	uint32_t* hist;   // [np]
 	uint4* deep;      // [kDeepPrefetch] {row base, r, m, -}
 	uint16_t* cls;    // [kWheelCls] alive classes: offsets o < 2431 (q = qa + o + 2431 i)
-	uint4* fac;       // [kMaxFactors] loop factors {f, barrett m, x, kind}: kind 0 tiny (x = shared address
-	                  // of its masks), 1 mid (x = -(2431^-1) mod f), 2 large
+	uint4* fac;       // [kMaxFactors] loop factors {f, barrett m, -(2431^-1) mod f (f < 37681), bit pattern}
 	const uint32_t* tab;  // the CTA's wheel tables
 	uint32_t tab0;        // ... as a shared address
 };
@@ -970,7 +1006,7 @@ __device__ __forceinline__ void wheel_drain(const SieveArgs& a, const WheelSmem&
 // nfl = the loop's factor slots in w.fac (odd prime factors of p other than
 // 11, 13, 17). Returns 1 + the deepest probe that killed in the segment (0: none).
 __device__ __forceinline__ uint32_t wheel_row(const SieveArgs& a, const WheelSmem& w, uint32_t lane,
-                                              const RowCtx& rc, uint32_t nfl)
+                                              const RowCtx& rc, uint32_t nfl, uint32_t nmid)
 {
 	const uint32_t qa = rc.qlo + 32 * rc.w0;
 	const uint64_t qe = uint64_t(rc.qlo) + 32ull * rc.w1 - 1;  // 64-bit: no 2^32 wrap
@@ -1071,25 +1107,22 @@ __device__ __forceinline__ uint32_t wheel_row(const SieveArgs& a, const WheelSme
 				const uint32_t c = w.cls[ci];
 				q0 = qa + c + kWheelChunk * k;
 				uint32_t nonc = evenm << (q0 & 1u);
-				for (uint32_t s = 0; s < nfl; ++s) {  // warp-uniform paths
+				// factors below 37681 (ascending, so they come first): the first i with f | q0 + 2431 i is
+				// (q0 mod f) g mod f; pattern = period-f mask below 32, a single bit above
+				for (uint32_t s = 0; s < nmid; ++s) {
+					const uint4 e = w.fac[s];  // {f, m, g, pattern}
+					nonc |= shl_clamp(e.w, mod_full(mod_lazy(q0, e.x, e.y) * e.z, e.x, e.y));
+				}
+				for (uint32_t s = nmid; s < nfl; ++s) {  // f >= 37681: at most two multiples of f in [q0, q0 + 31 * 2431]
 					const uint4 e = w.fac[s];
-					uint32_t t = mod_lazy(q0, e.x, e.y);
-					if (e.w == 0) {  // f < 32: masks of (f, t), t < 2f, in shared memory
-						uint32_t mk;
-						asm volatile("ld.shared.u32 %0, [%1];" : "=r"(mk) : "r"(e.z + 4 * t));
-						nonc |= mk;
-					} else if (e.w == 1) {  // first i with f | q0 + 2431 i is t g mod f; at most one below 32
-						nonc |= shl_clamp(1u, mod_full(t * e.z, e.x, e.y));
-					} else {  // f >= 37681: at most two multiples of f in [q0, q0 + 31 * 2431]
-						t = min(t, t - e.x);
-						uint32_t d = t ? e.x - t : 0u;
+					const uint32_t t = mod_full(q0, e.x, e.y);
+					uint32_t d = t ? e.x - t : 0u;
 #pragma unroll
-						for (int rep = 0; rep < 2; ++rep) {
-							const uint32_t i = __umulhi(min(d, kWheelChunk), kWheelDivMul);
-							nonc |= i * kWheelM == d ? shl_clamp(1u, i) : 0u;
-							d += e.x;  // < 2^32: f < 2^32 / 59 ... f <= p < 2^32 in TRIANGLE -> clamp below
-							if (d < e.x) d = kWheelChunk + 1;  // wrapped: no further multiple in reach
-						}
+					for (int rep = 0; rep < 2; ++rep) {
+						const uint32_t i = __umulhi(min(d, kWheelChunk), kWheelDivMul);
+						nonc |= i * kWheelM == d ? shl_clamp(1u, i) : 0u;
+						d += e.x;
+						if (d < e.x) d = kWheelChunk + 1;  // wrapped past 2^32: no further multiple in reach
 					}
 				}
 				alive = ~nonc;
@@ -1190,8 +1223,10 @@ __global__ void __launch_bounds__(kSieveThreads, 1) k_wsieve(const SieveArgs a)
 	const unsigned long long W = a.chunk_off[n_chunks];
 	const unsigned long long nwarps = static_cast<unsigned long long>(gridDim.x) * kSieveWarps;
 	const unsigned long long gw = static_cast<unsigned long long>(blockIdx.x) * kSieveWarps + wib;
-	unsigned long long ws = W * gw / nwarps;  // W < 2^40, nwarps < 2^20
-	const unsigned long long we = W * (gw + 1) / nwarps;
+	// W gw / nwarps without the 64-bit overflow of the product (units are 1/64 instruction here)
+	const unsigned long long Wq = W / nwarps, Wr = W % nwarps;
+	unsigned long long ws = Wq * gw + Wr * gw / nwarps;
+	const unsigned long long we = Wq * (gw + 1) + Wr * (gw + 1) / nwarps;
 
 	// 32-ary warp search: largest slot s with prefix(s) <= ws
 	uint32_t lo = 0, hi = a.n_slots;
@@ -1230,8 +1265,8 @@ __global__ void __launch_bounds__(kSieveThreads, 1) k_wsieve(const SieveArgs a)
 		const uint32_t head = __shfl_sync(kFull, fw, 0);
 		rc.nf = head & 0xffu;
 		rc.even = (head >> 8) & 1u;
-		rc.w0 = unit_window(a, u0, (head >> 16) & 3u, rc.wlast + 1);
-		rc.w1 = unit_window(a, u1, (head >> 16) & 3u, rc.wlast + 1);
+		rc.w0 = unit_window_mult(a, u0, head >> 16, rc.wlast + 1);
+		rc.w1 = unit_window_mult(a, u1, head >> 16, rc.wlast + 1);
 		if (rc.w1 <= rc.w0) continue;
 #pragma unroll
 		for (int k = 0; k < kMaxFactors; ++k) {
@@ -1243,19 +1278,16 @@ __global__ void __launch_bounds__(kSieveThreads, 1) k_wsieve(const SieveArgs a)
 		const bool keep = lane >= 1 && lane <= rc.nf && fw != 11 && fw != 13 && fw != 17;
 		const uint32_t keepm = __ballot_sync(kFull, keep);
 		if (keep) {
-			uint32_t x = 0, kind = 2;
-			if (fw < 32) {  // tiny: masks in shared memory
-				kind = 0;
-				x = w.tab0 + 4 * w.tab[kWtTinyOff + fw];
-			} else if (fw < kWheelMidMax) {
+			uint32_t x = 0;
+			if (fw < kWheelMidMax) {
 				// g = -(2431^-1) mod f; 143^-1 = (1 + f k) / 143 with k = (-f^-1) mod 143, likewise 17^-1
-				kind = 1;
 				const uint32_t i143 = (1 + fw * w.tab[kWtNinv143 + fw % 143]) / 143;
 				const uint32_t i17 = (1 + fw * w.tab[kWtNinv17 + fw % 17]) / 17;
 				x = fw - mod_full(i143 * i17, fw, fmv);
 			}
-			w.fac[__popc(keepm & ((1u << lane) - 1))] = make_uint4(fw, fmv, x, kind);
+			w.fac[__popc(keepm & ((1u << lane) - 1))] = make_uint4(fw, fmv, x, fw < 32 ? c_period_mask[fw] : 1u);
 		}
+		const uint32_t nmid = __popc(__ballot_sync(kFull, keep && fw < kWheelMidMax));
 		const uint32_t nfl = __popc(keepm);
 		// rows of the first deep probes, pulled into L1
 		if (kWheelReg + lane / 2 < a.np && lane < 2 * kDeepPrefetch) {
@@ -1267,7 +1299,7 @@ __global__ void __launch_bounds__(kSieveThreads, 1) k_wsieve(const SieveArgs a)
 		}
 		__syncwarp();
 
-		const uint32_t kk = wheel_row(a, w, lane, rc, nfl);
+		const uint32_t kk = wheel_row(a, w, lane, rc, nfl, nmid);
 		if (lane == 0 && kk) {
 			const uint32_t j = kk - 1;
 			const uint32_t killer = j < static_cast<uint32_t>(kWheelReg) ? std_prime(j) : __ldg(a.probes + j).x;
