@@ -165,7 +165,8 @@ struct cgpu_ctx {
 	DevBuf<uint4> derive_items;
 	DevBuf<uint32_t> wintab;
 	// wheel sieve (k_wsieve) for the standard probe sets: CUBOID_WHEEL=0 keeps k_sieve
-	bool wheel_enabled = true, wheel = false;
+	int wheel_mode = 1;  // CUBOID_WHEEL: 0 never, 1 for launches of long rows (kWheelMinWindows), 2 always
+	bool wheel = false;
 	DevBuf<uint32_t> wheeltab;
 	int wgrid = 0;
 	uint32_t row_cost_wheel = kDefaultRowCostWheel;
@@ -252,7 +253,7 @@ int cgpu_create(int device, void* stream, cgpu_ctx** out)
 	if (const char* rs = std::getenv("CUBOID_ROW_COST_SHORT"))
 		c->row_cost_short = static_cast<uint32_t>(std::atoi(rs));
 	if (const char* da = std::getenv("CUBOID_DRAIN_ALPHA")) c->drain_alpha = static_cast<float>(std::atof(da));
-	if (const char* wh = std::getenv("CUBOID_WHEEL")) c->wheel_enabled = std::atoi(wh) != 0;
+	if (const char* wh = std::getenv("CUBOID_WHEEL")) c->wheel_mode = std::atoi(wh);
 	if (const char* rw = std::getenv("CUBOID_ROW_COST_WHEEL")) c->row_cost_wheel = static_cast<uint32_t>(std::atoi(rw));
 	if (const char* wc = std::getenv("CUBOID_WHEEL_COSTS"))  // "base,mid,large,queued" instructions
 		std::sscanf(wc, "%f,%f,%f,%f", &c->wheel_cost[0], &c->wheel_cost[1], &c->wheel_cost[2], &c->wheel_cost[3]);
@@ -481,7 +482,7 @@ int finalize_set(cgpu_ctx* c, bool check_padding = false, bool keep_row0 = false
 		for (uint32_t j = 0; c->std_primes && j < c->nreg; ++j) c->std_primes = c->reg_r[j] == std_prime(j);
 	}
 	// k_wsieve needs the standard register probes and its shared memory (larger sets keep k_sieve)
-	c->wheel = c->std_primes && c->wheel_enabled && wsieve_smem_bytes(c->np) <= 220 * 1024;
+	c->wheel = c->std_primes && c->wheel_mode != 0 && wsieve_smem_bytes(c->np) <= 220 * 1024;
 	if (c->wheel) {  // wheel tables (11, 13, 17 as the wheel; strided window tables of 19..37)
 		CK(c->wheeltab.ensure(kWtWords));
 		CK(launch_wheeltab(c->ext.p, c->reg_base, c->wheeltab.p, c->stream));
@@ -982,8 +983,9 @@ int enqueue_sieve(cgpu_ctx* c, uint64_t p_lo, uint64_t q_start, uint64_t p_hi, u
 		a.short_rows = c->short_rows < 0 ? (mean_windows < kShortRowWindows ? 1u : 0u)
 		                                 : static_cast<uint32_t>(c->short_rows);
 		if (a.short_rows) a.row_cost = c->row_cost_short;  // the short-row kernel's own setup charge
+		// the wheel sieve pays a larger fixed cost per row: launches of short rows keep k_sieve
+		a.wheel = c->wheel && (c->wheel_mode >= 2 || mean_windows >= kWheelMinWindows) ? 1u : 0u;
 	}
-	a.wheel = c->wheel ? 1u : 0u;
 	a.wheeltab = c->wheeltab.p;
 	if (a.wheel) {
 		a.row_cost = c->row_cost_wheel;

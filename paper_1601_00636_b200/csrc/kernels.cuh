@@ -154,11 +154,19 @@ __host__ __device__ constexpr uint32_t wheel_tab_base(int j)  // first entry of 
 	return j <= kWheelFirst ? kWtTab : wheel_tab_base(j - 1) + 2 * std_prime(j - 1) * std_prime(j - 1);
 }
 constexpr uint32_t kWtWords = wheel_tab_base(kWheelReg);
+#ifndef CGPU_WHEEL_THREADS
+#define CGPU_WHEEL_THREADS 768
+#endif
+constexpr int kWheelThreads = CGPU_WHEEL_THREADS;  // one CTA per SM
+constexpr int kWheelWarps = kWheelThreads / 32;
 constexpr int kWheelQueue = 64;      // per-warp queue of single q alive after the register probes
 constexpr uint32_t kWheelCls = 2432; // per-warp list of alive classes (uint16 offsets below 2431)
 // k_wsieve's load-balance model (k_plan), in instructions, from the ncu instruction counts of C5:
 // per row segment, then per loop iteration {base, per factor below 37681, per factor above}, per queued q
-constexpr uint32_t kDefaultRowCostWheel = 1800 * 64;  // units of 1/64 instruction
+constexpr uint32_t kDefaultRowCostWheel = 200000;  // units of 1/64 instruction (1800 counted; sweep: 200000 best)
+// launches whose mean row has fewer 32-q windows keep k_sieve (C4, mean 1.6k: k_sieve 0.52 ms, k_wsieve 0.55;
+// C5, mean 6.3k: 3.02 -> 1.62 ms)
+constexpr uint32_t kWheelMinWindows = 3000;
 constexpr float kDefaultWheelCost[4] = {120.0f, 14.0f, 30.0f, 25.0f};
 
 struct SieveArgs {

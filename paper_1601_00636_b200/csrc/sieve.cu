@@ -1193,19 +1193,19 @@ __device__ __forceinline__ uint32_t wheel_row(const SieveArgs& a, const WheelSme
 }
 
 template <bool STOP>
-__global__ void __launch_bounds__(kSieveThreads, 1) k_wsieve(const SieveArgs a)
+__global__ void __launch_bounds__(kWheelThreads, 1) k_wsieve(const SieveArgs a)
 {
 	extern __shared__ uint4 s_dyn[];
 	__shared__ bool s_last;
-	__shared__ unsigned long long s_red[kSieveWarps];
+	__shared__ unsigned long long s_red[kWheelWarps];
 	const uint32_t lane = threadIdx.x & 31;
 	const uint32_t wib = threadIdx.x >> 5;
 	WheelSmem w;
 	uint4* deep_all = s_dyn;
-	uint4* fac_all = deep_all + kSieveWarps * kDeepPrefetch;
-	uint32_t* q_all = reinterpret_cast<uint32_t*>(fac_all + kSieveWarps * kMaxFactors);
-	uint16_t* cls_all = reinterpret_cast<uint16_t*>(q_all + kSieveWarps * kWheelQueue);
-	uint32_t* s_tab = reinterpret_cast<uint32_t*>(cls_all + kSieveWarps * kWheelCls);
+	uint4* fac_all = deep_all + kWheelWarps * kDeepPrefetch;
+	uint32_t* q_all = reinterpret_cast<uint32_t*>(fac_all + kWheelWarps * kMaxFactors);
+	uint16_t* cls_all = reinterpret_cast<uint16_t*>(q_all + kWheelWarps * kWheelQueue);
+	uint32_t* s_tab = reinterpret_cast<uint32_t*>(cls_all + kWheelWarps * kWheelCls);
 	uint32_t* h_all = s_tab + kWtWords;
 	w.deep = deep_all + wib * kDeepPrefetch;
 	w.fac = fac_all + wib * kMaxFactors;
@@ -1221,8 +1221,8 @@ __global__ void __launch_bounds__(kSieveThreads, 1) k_wsieve(const SieveArgs a)
 
 	const uint32_t n_chunks = plan_chunks(a.n_slots);
 	const unsigned long long W = a.chunk_off[n_chunks];
-	const unsigned long long nwarps = static_cast<unsigned long long>(gridDim.x) * kSieveWarps;
-	const unsigned long long gw = static_cast<unsigned long long>(blockIdx.x) * kSieveWarps + wib;
+	const unsigned long long nwarps = static_cast<unsigned long long>(gridDim.x) * kWheelWarps;
+	const unsigned long long gw = static_cast<unsigned long long>(blockIdx.x) * kWheelWarps + wib;
 	// W gw / nwarps without the 64-bit overflow of the product (units are 1/64 instruction here)
 	const unsigned long long Wq = W / nwarps, Wr = W % nwarps;
 	unsigned long long ws = Wq * gw + Wr * gw / nwarps;
@@ -1313,7 +1313,7 @@ __global__ void __launch_bounds__(kSieveThreads, 1) k_wsieve(const SieveArgs a)
 	__syncthreads();
 	for (uint32_t j = threadIdx.x; j < a.np; j += blockDim.x) {
 		unsigned long long s = 0;
-		for (int v = 0; v < kSieveWarps; ++v) s += h_all[static_cast<size_t>(v) * a.np + j];
+		for (int v = 0; v < kWheelWarps; ++v) s += h_all[static_cast<size_t>(v) * a.np + j];
 		if (s) atomicAdd(&a.hist[__ldg(a.probe_rank + j)], s);
 	}
 	__threadfence();
@@ -1330,7 +1330,7 @@ __global__ void __launch_bounds__(kSieveThreads, 1) k_wsieve(const SieveArgs a)
 	__syncthreads();
 	if (threadIdx.x == 0) {
 		unsigned long long t = 0;
-		for (int v = 0; v < kSieveWarps; ++v) t += s_red[v];
+		for (int v = 0; v < kWheelWarps; ++v) t += s_red[v];
 		a.counters[0] = t + *reinterpret_cast<volatile unsigned long long*>(a.counters + 1);
 		a.tickets[1] = 0;
 	}
@@ -1516,9 +1516,9 @@ int sieve_grid(int device, int nr2, int nr3, bool std_primes, size_t smem)
 
 __host__ __device__ size_t wsieve_smem_bytes(uint32_t np)
 {
-	return sizeof(uint4) * kSieveWarps * (kDeepPrefetch + kMaxFactors) + sizeof(uint32_t) * kSieveWarps * kWheelQueue +
-	       sizeof(uint16_t) * kSieveWarps * kWheelCls + sizeof(uint32_t) * kWtWords +
-	       sizeof(uint32_t) * static_cast<size_t>(np) * kSieveWarps;
+	return sizeof(uint4) * kWheelWarps * (kDeepPrefetch + kMaxFactors) + sizeof(uint32_t) * kWheelWarps * kWheelQueue +
+	       sizeof(uint16_t) * kWheelWarps * kWheelCls + sizeof(uint32_t) * kWtWords +
+	       sizeof(uint32_t) * static_cast<size_t>(np) * kWheelWarps;
 }
 
 int wsieve_grid(int device, size_t smem)
@@ -1532,7 +1532,7 @@ int wsieve_grid(int device, size_t smem)
 		cudaFuncGetAttributes(&fa, f);
 		cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - static_cast<int>(fa.sharedSizeBytes));
 	}
-	cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, variants[0], kSieveThreads, smem);
+	cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, variants[0], kWheelThreads, smem);
 	if (per_sm < 1) per_sm = 1;
 	return sms * per_sm;
 }
@@ -1557,7 +1557,7 @@ cudaError_t launch_sieve(const SieveArgs& a, int grid, cudaStream_t s)
 	void* args[] = {const_cast<SieveArgs*>(&a)};
 	if (a.wheel)
 		return cudaLaunchKernel(a.stop != nullptr ? wsieve_fn<true>() : wsieve_fn<false>(), dim3(grid),
-		                        dim3(kSieveThreads), args, wsieve_smem_bytes(a.np), s);
+		                        dim3(kWheelThreads), args, wsieve_smem_bytes(a.np), s);
 	return cudaLaunchKernel(sieve_kernel_ptr(static_cast<int>(a.nreg2), static_cast<int>(a.nreg3), a.std_primes,
 	                                         a.stop != nullptr, a.short_rows != 0),
 	                        dim3(grid),

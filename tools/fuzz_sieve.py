@@ -1,8 +1,8 @@
 """Randomised parity sweep of the device sieve against the C oracle (a tool,
 not part of the -m gpu suite): random prime sets (standard 11..37 heads and
 generic ones, with and without 3, 5, 7), random TRIANGLE and REGION ranges
-with mid-row starts, both loop-variant sets (CUBOID_SHORT_ROWS forced per
-context), random block-cyclic shards. Prints one line per case and a summary.
+with mid-row starts, both loop-variant sets of k_sieve (CUBOID_SHORT_ROWS forced per
+context) and the wheel sieve k_wsieve (CUBOID_WHEEL=2), random block-cyclic shards. Prints one line per case and a summary.
 
     python tools/fuzz_sieve.py [seconds] [seed]
 """
@@ -24,8 +24,9 @@ def main():
     budget = float(sys.argv[1]) if len(sys.argv) > 1 else 120.0
     rng = random.Random(int(sys.argv[2]) if len(sys.argv) > 2 else 7)
     devs = {}
-    for sr in ("0", "1"):
-        os.environ["CUBOID_SHORT_ROWS"] = sr
+    for sr in ("0", "1", "w"):  # "w": the wheel sieve forced on every standard-set launch
+        os.environ["CUBOID_SHORT_ROWS"] = "0" if sr == "w" else sr
+        os.environ["CUBOID_WHEEL"] = "2" if sr == "w" else "0"
         devs[sr] = Device(0)
     t0, n, bad = time.time(), 0, 0
     while time.time() - t0 < budget:
@@ -38,7 +39,7 @@ def main():
         else:
             P = sorted(rng.sample(primes_in_range(11, 300), rng.randrange(1, 6)))
         tb, offs = port.build_set(P)
-        sr = rng.choice(["0", "1"])
+        sr = rng.choice(["0", "1", "w", "w"])
         dev = devs[sr]
         dev.load(P, tb)
         mode = rng.choice([N.TRIANGLE, N.REGION])
