@@ -627,18 +627,19 @@ def run_ours(args, wl, primes):
     opp, d_eff, omega_bar = ops_per_pair(primes, killable, hist, survivors, pairs,
                                          wl["p_lo"], wl["p_hi"])
     kavg = float(np.mean(kern_ms))
+    kname = dev.sieve_kernel() or "k_sieve"  # the wheel sieve k_wsieve for C5, the window sieve otherwise
     achieved = local_pairs * opp / (kavg * 1e-3)
     traffic = None
     prof = os.path.join(ROOT, "profiles", "ncu_summary.json")
     if os.path.exists(prof):
         try:
-            traffic = json.load(open(prof)).get("k_sieve", {}).get(wl["desc"][:2], {}).get("dram_bytes")
+            traffic = json.load(open(prof)).get(kname, {}).get(wl["desc"][:2], {}).get("dram_bytes")
         except (ValueError, AttributeError):
             traffic = None
     ncu = None
     if os.path.exists(prof):
         try:
-            x = json.load(open(prof)).get("k_sieve", {}).get(wl["desc"][:2], {})
+            x = json.load(open(prof)).get(kname, {}).get(wl["desc"][:2], {})
             ncu = {k: x.get(k) for k in ("round", "duration_ms", "issue_active_pct", "alu_pipe_pct",
                                           "xu_pipe_pct", "lsu_pipe_pct", "l1tex_throughput_pct",
                                           "smem_wavefront_pct", "fma_pipe_pct", "warps_active_pct",
@@ -655,7 +656,7 @@ def run_ours(args, wl, primes):
     # holds its share of the instructions (scaled by its pairs).
     sms = torch.cuda.get_device_properties(local).multi_processor_count
     clocks = clk.summary()
-    nk = (json.load(open(prof)).get("k_sieve", {}).get(wl["desc"][:2], {})
+    nk = (json.load(open(prof)).get(kname, {}).get(wl["desc"][:2], {})
           if os.path.exists(prof) else {})
     share = local_pairs / max(pairs, 1)
     hw = {}
@@ -668,7 +669,7 @@ def run_ours(args, wl, primes):
     roof = {"bound": "int32_issue", "achieved": hw.get("achieved"), "peak": int_peak["best"],
             "unit": "thread-instructions/s", "frac": hw.get("frac"), "traffic": traffic,
             "smem_wavefront_frac": hw.get("smem_wavefront_frac"),
-            "kernel": "k_sieve", "kernel_ms": kavg, "pairs_per_launch": local_pairs,
+            "kernel": kname, "kernel_ms": kavg, "pairs_per_launch": local_pairs,
             "warp_inst_per_launch": nk.get("warp_inst", 0) * share or None,
             "smem_wavefronts_per_launch": nk.get("smem_wavefronts", 0) * share or None,
             "ncu_round": nk.get("round"), "sms": sms,

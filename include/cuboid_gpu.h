@@ -238,6 +238,13 @@ int cgpu_set_stop_word(cgpu_ctx* ctx, uint32_t* word);
  * ms[2] = both. */
 int cgpu_last_timings(cgpu_ctx* ctx, float* ms3);
 
+/* Name of the sieve kernel the last launch ran: "k_wsieve" (the wheel sieve:
+ * standard probe sets, launches of long rows) or "k_sieve" (the window sieve);
+ * "" before the first launch. Results never depend on the choice
+ * (CUBOID_WHEEL = 0 / 1 / 2: never / by mean row length / always). No
+ * reference counterpart: profiling and the bench's roofline read it. */
+const char* cgpu_last_sieve_kernel(cgpu_ctx* ctx);
+
 /* Measured INT32 throughput of `device` in thread-ops/s: ops4[0] = LOP3 chains
  * (ALU pipe), ops4[1] = IMAD chains (FMA pipe), ops4[2] = IMAD + LOP3
  * interleaved (3 register sources each), ops4[3] = IMAD + LOP3 with

@@ -62,6 +62,7 @@ SIGNATURES = {
                                   C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p,
                                   C.c_uint64]),
     "cgpu_last_timings": (C.c_int, [C.c_void_p, C.POINTER(C.c_float)]),
+    "cgpu_last_sieve_kernel": (C.c_char_p, [C.c_void_p]),
     "cgpu_multi_create": (C.c_int, [C.c_int, C.c_void_p, C.POINTER(C.c_void_p)]),
     "cgpu_multi_destroy": (C.c_int, [C.c_void_p]),
     "cgpu_multi_size": (C.c_int, [C.c_void_p, C.POINTER(C.c_int)]),

@@ -194,7 +194,7 @@ struct cgpu_ctx {
 	DevBuf<uint32_t> tickets, rowfac;
 	DevBuf<uint32_t> d_probe_rank;
 	DevBuf<uint32_t> block_rmax;
-	bool launched = false, results_internal = false, timed = false;
+	bool launched = false, results_internal = false, timed = false, last_wheel = false;
 	uint64_t last_nblocks = 0, last_surv_cap = 0;
 	cudaEvent_t ev[3] = {};
 	float timings[3] = {};
@@ -1047,6 +1047,7 @@ int enqueue_sieve(cgpu_ctx* c, uint64_t p_lo, uint64_t q_start, uint64_t p_hi, u
 	c->timed = true;
 	c->last_nblocks = nblocks;
 	c->last_surv_cap = surv_cap;
+	c->last_wheel = a.wheel != 0;
 	c->launched = true;
 	return CGPU_OK;
 }
@@ -1250,6 +1251,12 @@ int cgpu_sieve(cgpu_ctx* c, uint64_t p_lo, uint64_t q_start, uint64_t p_hi, int 
 {
 	if (int rc = cgpu_sieve_launch(c, p_lo, q_start, p_hi, mode, G, g, surv_pq ? surv_cap : 0)) return rc;
 	return cgpu_sieve_results(c, counts, hist, block_rmax, block_cap, surv_pq, surv_cap);
+}
+
+const char* cgpu_last_sieve_kernel(cgpu_ctx* c)
+{
+	if (!c || !c->launched) return "";
+	return c->last_wheel ? "k_wsieve" : "k_sieve";
 }
 
 int cgpu_last_timings(cgpu_ctx* c, float* ms3)

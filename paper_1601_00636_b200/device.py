@@ -171,6 +171,10 @@ class Device:
         N.check(N.lib().cgpu_last_timings(self._ctx, t))
         return {"plan": t[0], "sieve": t[1], "total": t[2]}
 
+    def sieve_kernel(self) -> str:
+        """The kernel the last sieve launch ran ("k_wsieve" or "k_sieve")."""
+        return N.lib().cgpu_last_sieve_kernel(self._ctx).decode()
+
     def launch_count(self) -> int:
         n = C.c_uint32()
         N.check(N.lib().cgpu_last_launch_count(self._ctx, C.byref(n)))
