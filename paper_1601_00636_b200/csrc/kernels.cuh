@@ -155,19 +155,23 @@ __host__ __device__ constexpr uint32_t wheel_tab_base(int j)  // first entry of 
 }
 constexpr uint32_t kWtWords = wheel_tab_base(kWheelReg);
 #ifndef CGPU_WHEEL_THREADS
-#define CGPU_WHEEL_THREADS 768
+#define CGPU_WHEEL_THREADS 1024
 #endif
-constexpr int kWheelThreads = CGPU_WHEEL_THREADS;  // one CTA per SM
+constexpr int kWheelThreads = CGPU_WHEEL_THREADS;  // one 32-warp CTA per SM at 64 registers (768 x 80: C5 1.66 ms,
+                                                   // 896 x 72: 1.64, 1024 x 64: 1.57 -- the loop is latency-bound)
 constexpr int kWheelWarps = kWheelThreads / 32;
 constexpr int kWheelQueue = 64;      // per-warp queue of single q alive after the register probes
-constexpr uint32_t kWheelCls = 2432; // per-warp list of alive classes (uint16 offsets below 2431)
+#ifndef CGPU_WHEEL_CLS
+#define CGPU_WHEEL_CLS 1216
+#endif
+constexpr uint32_t kWheelCls = CGPU_WHEEL_CLS;  // per-warp list of alive classes (uint16 offsets below 2431), one batch
 // k_wsieve's load-balance model (k_plan), in instructions, from the ncu instruction counts of C5:
 // per row segment, then per loop iteration {base, per factor below 37681, per factor above}, per queued q
-constexpr uint32_t kDefaultRowCostWheel = 200000;  // units of 1/64 instruction (1800 counted; sweep: 200000 best)
-// launches whose mean row has fewer 32-q windows keep k_sieve (C4, mean 1.6k: k_sieve 0.52 ms, k_wsieve 0.55;
-// C5, mean 6.3k: 3.02 -> 1.62 ms)
-constexpr uint32_t kWheelMinWindows = 3000;
-constexpr float kDefaultWheelCost[4] = {120.0f, 14.0f, 30.0f, 25.0f};
+constexpr uint32_t kDefaultRowCostWheel = 160000;  // units of 1/64 instruction (1800 instructions counted; sweep: 2500 best)
+// launches whose mean row has fewer 32-q windows keep k_sieve (TRIANGLE p <= 5e4, mean 780: k_sieve 0.19 ms,
+// k_wsieve 0.25; C4, mean 1.6k: 0.52 / 0.50; 5e4 < p <= 1.5e5, mean 3.1k: 0.86 / 0.59; C5, mean 6.3k: 3.02 / 1.55)
+constexpr uint32_t kWheelMinWindows = 1500;
+constexpr float kDefaultWheelCost[4] = {140.0f, 14.0f, 30.0f, 25.0f};
 
 struct SieveArgs {
 	const uint32_t* ext;          // row-extended tables

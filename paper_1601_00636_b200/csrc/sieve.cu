@@ -887,7 +887,8 @@ struct WheelSmem {
 	uint32_t* queue;  // [kWheelQueue] q alive after the register probes
 	uint32_t* hist;   // [np]
 	uint4* deep;      // [kDeepPrefetch] {row base, r, m, -}
-	uint16_t* cls;    // [kWheelCls] alive classes: offsets o < 2431 (q = qa + o + 2431 i)
+	uint16_t* cls;    // [kWheelCls] alive classes of the current batch: offsets o < 2431 (q = qa + o + 2431 i)
+	uint16_t* l143;   // [192] alive offsets mod 143 at [0, 143), mod 17 at [160, 177)
 	uint4* fac;       // [kMaxFactors] loop factors {f, barrett m, -(2431^-1) mod f (f < 37681), bit pattern}
 	const uint32_t* tab;  // the CTA's wheel tables
 	uint32_t tab0;        // ... as a shared address
@@ -1034,7 +1035,7 @@ __device__ __forceinline__ uint32_t wheel_row(const SieveArgs& a, const WheelSme
 		const uint32_t x11 = mod_full(qa11 + c, 11, barrett_m(11)), x13 = mod_full(qa13 + c, 13, barrett_m(13));
 		const bool ok = c < 143 && !((kill11 >> x11) & 1u) && !((kill13 >> x13) & 1u);
 		const uint32_t bal = __ballot_sync(kFull, ok);
-		if (ok) w.cls[kWheelCls - 192 + n143 + __popc(bal & lt)] = static_cast<uint16_t>(c);
+		if (ok) w.l143[n143 + __popc(bal & lt)] = static_cast<uint16_t>(c);
 		n143 += __popc(bal);
 	}
 	uint32_t n17;
@@ -1042,46 +1043,35 @@ __device__ __forceinline__ uint32_t wheel_row(const SieveArgs& a, const WheelSme
 		const uint32_t x17 = mod_full(qa17 + lane, 17, barrett_m(17));
 		const bool ok = lane < 17 && !((kill17 >> x17) & 1u);
 		const uint32_t bal = __ballot_sync(kFull, ok);
-		if (ok) w.cls[kWheelCls - 32 + __popc(bal & lt)] = static_cast<uint16_t>(lane);
+		if (ok) w.l143[160 + __popc(bal & lt)] = static_cast<uint16_t>(lane);
 		n17 = __popc(bal);
 	}
 	__syncwarp();
-	uint32_t n = 0;
-	{
-		// The staging lists sit in the top 192 entries of cls; a full product (143 x 17 = 2431 > 2240)
-		// would overwrite them, so they are first copied to registers: lane l holds L143[l + 32 m]
-		// (m < 5) and L17[l] and the combinations are formed with shuffles.
-		uint32_t l143[5], l17;
-#pragma unroll
-		for (int m = 0; m < 5; ++m) l143[m] = (32 * m + lane < n143) ? w.cls[kWheelCls - 192 + 32 * m + lane] : 0u;
-		l17 = lane < n17 ? w.cls[kWheelCls - 32 + lane] : 0u;
-		__syncwarp();
-		const uint32_t ntot = n143 * n17;
-		const uint32_t rcp17 = 65536u / max(n17, 1u) + 1;  // floor(ci / n17) = (ci * rcp17) >> 16 for ci < 2432
-		for (uint32_t c0 = 0; c0 < ntot; c0 += 32) {
-			const uint32_t ci = c0 + lane;
-			const uint32_t i143 = (ci * rcp17) >> 16, i17 = ci - i143 * n17;
-			uint32_t o143 = 0;
-#pragma unroll
-			for (int m = 0; m < 5; ++m) {
-				const uint32_t v = __shfl_sync(kFull, l143[m], i143 & 31);
-				if ((i143 >> 5) == static_cast<uint32_t>(m)) o143 = v;
-			}
-			const uint32_t o17 = __shfl_sync(kFull, l17, i17 & 31);
-			const uint32_t o = mod_full(o143 * kWheelE143 + o17 * kWheelE17, kWheelM, barrett_m(kWheelM));
-			const bool ok = ci < ntot && o <= span;
-			const uint32_t bal = __ballot_sync(kFull, ok);
-			if (ok) w.cls[n + __popc(bal & lt)] = static_cast<uint16_t>(o);
-			n += __popc(bal);
-		}
-	}
-	__syncwarp();
-
 	// S[j - kWheelFirst] = sum of popc(alive before register probe j), j = 3..7
 	uint32_t S[kWheelReg - kWheelFirst];
 #pragma unroll
 	for (int j = 0; j < kWheelReg - kWheelFirst; ++j) S[j] = 0;
 	uint32_t entered = 0, qn = 0;
+	const uint32_t ntot = n143 * n17;
+	const uint32_t rcp17 = 65536u / max(n17, 1u) + 1;  // floor(ci / n17) = (ci * rcp17) >> 16 for ci < 2432
+
+	// the alive classes o < 2431 (CRT combinations of the two lists) with o <= span, kWheelCls at a
+	// time (a canonical row has 135; only rows that 11 and 17 both divide exceed one batch)
+	for (uint32_t cb = 0; cb < ntot; cb += kWheelCls) {
+	const uint32_t cend = min(cb + kWheelCls, ntot);
+	uint32_t n = 0;
+	for (uint32_t c0 = cb; c0 < cend; c0 += 32) {
+		const uint32_t ci = c0 + lane;
+		const uint32_t i143 = (ci * rcp17) >> 16, i17 = ci - i143 * n17;
+		uint32_t o = kWheelM;
+		if (ci < cend)
+			o = mod_full(w.l143[i143] * kWheelE143 + w.l143[160 + i17] * kWheelE17, kWheelM, barrett_m(kWheelM));
+		const bool ok = ci < cend && o <= span;
+		const uint32_t bal = __ballot_sync(kFull, ok);
+		if (ok) w.cls[n + __popc(bal & lt)] = static_cast<uint16_t>(o);
+		n += __popc(bal);
+	}
+	__syncwarp();
 
 	if (n) {
 		// shared address of row (p mod r) of each strided window table
@@ -1175,6 +1165,8 @@ __device__ __forceinline__ uint32_t wheel_row(const SieveArgs& a, const WheelSme
 			if (last) break;
 		}
 	}
+	__syncwarp();
+	}  // class batches
 	// first-kill counts of the register probes
 	uint32_t tot[kWheelReg + 1];
 	wheel_counts(rc, w, lane, qa, qb, a11, a13, tot[0], tot[1], tot[2]);
@@ -1205,12 +1197,14 @@ __global__ void __launch_bounds__(kWheelThreads, 1) k_wsieve(const SieveArgs a)
 	uint4* fac_all = deep_all + kWheelWarps * kDeepPrefetch;
 	uint32_t* q_all = reinterpret_cast<uint32_t*>(fac_all + kWheelWarps * kMaxFactors);
 	uint16_t* cls_all = reinterpret_cast<uint16_t*>(q_all + kWheelWarps * kWheelQueue);
-	uint32_t* s_tab = reinterpret_cast<uint32_t*>(cls_all + kWheelWarps * kWheelCls);
+	uint16_t* l_all = cls_all + kWheelWarps * kWheelCls;
+	uint32_t* s_tab = reinterpret_cast<uint32_t*>(l_all + kWheelWarps * 192);
 	uint32_t* h_all = s_tab + kWtWords;
 	w.deep = deep_all + wib * kDeepPrefetch;
 	w.fac = fac_all + wib * kMaxFactors;
 	w.queue = q_all + wib * kWheelQueue;
 	w.cls = cls_all + wib * kWheelCls;
+	w.l143 = l_all + wib * 192;
 	w.hist = h_all + static_cast<size_t>(wib) * a.np;
 	w.tab = s_tab;
 	w.tab0 = static_cast<uint32_t>(__cvta_generic_to_shared(s_tab));
@@ -1517,7 +1511,7 @@ int sieve_grid(int device, int nr2, int nr3, bool std_primes, size_t smem)
 __host__ __device__ size_t wsieve_smem_bytes(uint32_t np)
 {
 	return sizeof(uint4) * kWheelWarps * (kDeepPrefetch + kMaxFactors) + sizeof(uint32_t) * kWheelWarps * kWheelQueue +
-	       sizeof(uint16_t) * kWheelWarps * kWheelCls + sizeof(uint32_t) * kWtWords +
+	       sizeof(uint16_t) * kWheelWarps * (kWheelCls + 192) + sizeof(uint32_t) * kWtWords +
 	       sizeof(uint32_t) * static_cast<size_t>(np) * kWheelWarps;
 }
 
