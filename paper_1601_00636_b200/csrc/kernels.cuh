@@ -154,6 +154,7 @@ __host__ __device__ constexpr uint32_t wheel_tab_base(int j)  // first entry of 
 	return j <= kWheelFirst ? kWtTab : wheel_tab_base(j - 1) + 2 * std_prime(j - 1) * std_prime(j - 1);
 }
 constexpr uint32_t kWtWords = wheel_tab_base(kWheelReg);
+constexpr uint32_t kWtBytes = (4 * kWtWords + 15) / 16 * 16;  // the per-warp blocks after them stay 16-byte aligned
 #ifndef CGPU_WHEEL_THREADS
 #define CGPU_WHEEL_THREADS 1024
 #endif
@@ -167,6 +168,14 @@ constexpr int kWheelQueue = 64;      // per-warp queue of single q alive after t
 constexpr uint32_t kWheelCls = CGPU_WHEEL_CLS;  // per-warp list of alive classes (uint16 offsets below 2431), one batch
 // k_wsieve's load-balance model (k_plan), in instructions, from the ncu instruction counts of C5:
 // per row segment, then per loop iteration {base, per factor below 37681, per factor above}, per queued q
+// per-warp shared-memory block of k_wsieve (byte offsets): deep-probe rows, loop factors, the q
+// queue, the two alive-offset lists, the class list of the current batch, the first-kill counters
+constexpr uint32_t kWbFac = 16 * 8;                          // after uint4 deep[kDeepPrefetch = 8]
+constexpr uint32_t kWbQueue = kWbFac + 16 * kMaxFactors;
+constexpr uint32_t kWbLists = kWbQueue + 4 * kWheelQueue;
+constexpr uint32_t kWbCls = kWbLists + 2 * 192;
+constexpr uint32_t kWbHist = (kWbCls + 2 * kWheelCls + 15) / 16 * 16;
+__host__ __device__ constexpr uint32_t wheel_warp_bytes(uint32_t np) { return (kWbHist + 4 * np + 15) / 16 * 16; }
 constexpr uint32_t kDefaultRowCostWheel = 160000;  // units of 1/64 instruction (1800 instructions counted; sweep: 2500 best)
 // launches whose mean row has fewer 32-q windows keep k_sieve (TRIANGLE p <= 5e4, mean 780: k_sieve 0.19 ms,
 // k_wsieve 0.25; C4, mean 1.6k: 0.52 / 0.50; 5e4 < p <= 1.5e5, mean 3.1k: 0.86 / 0.59; C5, mean 6.3k: 3.02 / 1.55)

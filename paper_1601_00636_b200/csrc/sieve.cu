@@ -1087,11 +1087,17 @@ __device__ __forceinline__ uint32_t wheel_row(const SieveArgs& a, const WheelSme
 		const uint32_t n_iter = (total + 31) / 32;
 		const uint32_t kfull = (span + 1) / kWheelChunk;  // chunks lying wholly inside the segment
 		const uint32_t n_full = (n * kfull) / 32;
-		uint32_t k = lane / n, ci = lane - k * n;
-		const uint32_t dk = 32 / n, dc = 32 - dk * n;
+		uint32_t k = 0, ci = lane;
+		while (ci >= n) {
+			ci -= n;
+			++k;
+		}
 
-		for (uint32_t it = 0;; ++it) {
-			const bool last = it >= n_iter;  // one more pass to drain what is left in the queue
+		// `left` counts the iterations down; the last n_edge of them touch the row's partial windows
+		// or lanes past the end, and one more pass drains what is left in the queue
+		const uint32_t n_edge = n_iter - n_full;
+		for (uint32_t left = n_iter;; --left) {
+			const bool last = left == 0;
 			uint32_t alive = 0, q0 = 0;
 			if (!last) {
 				const uint32_t c = w.cls[ci];
@@ -1099,10 +1105,12 @@ __device__ __forceinline__ uint32_t wheel_row(const SieveArgs& a, const WheelSme
 				uint32_t nonc = evenm << (q0 & 1u);
 				// factors below 37681 (ascending, so they come first): the first i with f | q0 + 2431 i is
 				// (q0 mod f) g mod f; pattern = period-f mask below 32, a single bit above
-				for (uint32_t s = 0; s < nmid; ++s) {
+#pragma unroll 1
+				for (uint32_t s = 0; s < nmid; ++s) {  // (not unrolled: 1.7 factors on average, code size)
 					const uint4 e = w.fac[s];  // {f, m, g, pattern}
 					nonc |= shl_clamp(e.w, mod_full(mod_lazy(q0, e.x, e.y) * e.z, e.x, e.y));
 				}
+#pragma unroll 1
 				for (uint32_t s = nmid; s < nfl; ++s) {  // f >= 37681: at most two multiples of f in [q0, q0 + 31 * 2431]
 					const uint4 e = w.fac[s];
 					const uint32_t t = mod_full(q0, e.x, e.y);
@@ -1116,7 +1124,7 @@ __device__ __forceinline__ uint32_t wheel_row(const SieveArgs& a, const WheelSme
 					}
 				}
 				alive = ~nonc;
-				if (it >= n_full) {  // edge: the row's last chunks and lanes past the end
+				if (left <= n_edge) {  // edge: the row's last chunks and lanes past the end
 					uint32_t vm = 0;
 					if (k < nchunk) {
 						const uint32_t rem = span - kWheelChunk * k;
@@ -1134,9 +1142,8 @@ __device__ __forceinline__ uint32_t wheel_row(const SieveArgs& a, const WheelSme
 					alive &= ~M;
 					if (j + 1 < kWheelReg) S[j + 1 - kWheelFirst] += __popc(alive);
 				}
-				ci += dc;
-				k += dk;
-				if (ci >= n) {
+				ci += 32;  // next window of the lane: 32 classes on (a batch of fewer than 32 wraps more than once)
+				while (ci >= n) {
 					ci -= n;
 					++k;
 				}
@@ -1192,20 +1199,19 @@ __global__ void __launch_bounds__(kWheelThreads, 1) k_wsieve(const SieveArgs a)
 	__shared__ unsigned long long s_red[kWheelWarps];
 	const uint32_t lane = threadIdx.x & 31;
 	const uint32_t wib = threadIdx.x >> 5;
+	// shared memory: the wheel tables, then one contiguous block per warp (a single base address
+	// with constant offsets: separate per-type arrays made the 64-register loop recompute five
+	// addresses from the thread index every iteration)
 	WheelSmem w;
-	uint4* deep_all = s_dyn;
-	uint4* fac_all = deep_all + kWheelWarps * kDeepPrefetch;
-	uint32_t* q_all = reinterpret_cast<uint32_t*>(fac_all + kWheelWarps * kMaxFactors);
-	uint16_t* cls_all = reinterpret_cast<uint16_t*>(q_all + kWheelWarps * kWheelQueue);
-	uint16_t* l_all = cls_all + kWheelWarps * kWheelCls;
-	uint32_t* s_tab = reinterpret_cast<uint32_t*>(l_all + kWheelWarps * 192);
-	uint32_t* h_all = s_tab + kWtWords;
-	w.deep = deep_all + wib * kDeepPrefetch;
-	w.fac = fac_all + wib * kMaxFactors;
-	w.queue = q_all + wib * kWheelQueue;
-	w.cls = cls_all + wib * kWheelCls;
-	w.l143 = l_all + wib * 192;
-	w.hist = h_all + static_cast<size_t>(wib) * a.np;
+	uint32_t* s_tab = reinterpret_cast<uint32_t*>(s_dyn);
+	const uint32_t wstride = wheel_warp_bytes(a.np);
+	unsigned char* blk = (reinterpret_cast<unsigned char*>(s_tab) + kWtBytes) + static_cast<size_t>(wib) * wstride;
+	w.deep = reinterpret_cast<uint4*>(blk);
+	w.fac = reinterpret_cast<uint4*>(blk + kWbFac);
+	w.queue = reinterpret_cast<uint32_t*>(blk + kWbQueue);
+	w.l143 = reinterpret_cast<uint16_t*>(blk + kWbLists);
+	w.cls = reinterpret_cast<uint16_t*>(blk + kWbCls);
+	w.hist = reinterpret_cast<uint32_t*>(blk + kWbHist);
 	w.tab = s_tab;
 	w.tab0 = static_cast<uint32_t>(__cvta_generic_to_shared(s_tab));
 	for (uint32_t j = lane; j < a.np; j += 32) w.hist[j] = 0;
@@ -1307,7 +1313,9 @@ __global__ void __launch_bounds__(kWheelThreads, 1) k_wsieve(const SieveArgs a)
 	__syncthreads();
 	for (uint32_t j = threadIdx.x; j < a.np; j += blockDim.x) {
 		unsigned long long s = 0;
-		for (int v = 0; v < kWheelWarps; ++v) s += h_all[static_cast<size_t>(v) * a.np + j];
+		for (int v = 0; v < kWheelWarps; ++v)
+			s += reinterpret_cast<const uint32_t*>((reinterpret_cast<unsigned char*>(s_tab) + kWtBytes) +
+			                                       static_cast<size_t>(v) * wstride + kWbHist)[j];
 		if (s) atomicAdd(&a.hist[__ldg(a.probe_rank + j)], s);
 	}
 	__threadfence();
@@ -1510,9 +1518,7 @@ int sieve_grid(int device, int nr2, int nr3, bool std_primes, size_t smem)
 
 __host__ __device__ size_t wsieve_smem_bytes(uint32_t np)
 {
-	return sizeof(uint4) * kWheelWarps * (kDeepPrefetch + kMaxFactors) + sizeof(uint32_t) * kWheelWarps * kWheelQueue +
-	       sizeof(uint16_t) * kWheelWarps * (kWheelCls + 192) + sizeof(uint32_t) * kWtWords +
-	       sizeof(uint32_t) * static_cast<size_t>(np) * kWheelWarps;
+	return kWtBytes + static_cast<size_t>(kWheelWarps) * wheel_warp_bytes(np);
 }
 
 int wsieve_grid(int device, size_t smem)
