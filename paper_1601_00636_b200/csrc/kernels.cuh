@@ -149,10 +149,15 @@ constexpr uint32_t kWtTinyOff = 1856;  // [32] f -> word offset of the tiny-fact
 constexpr uint32_t kWtTiny = 1888;     // masks (f, t), t < 2f: bits i with f | t + 2431 i   (234 words)
 constexpr uint32_t kWtTab = 2144;    // strided window tables of 19..37: entry (j, a, b), b < 2r:
                                      // bit i = u_r(a, (b + 2431 i) mod r)
-__host__ __device__ constexpr uint32_t wheel_tab_base(int j)  // first entry of register probe j >= kWheelFirst
+// first entry of register probe j >= kWheelFirst. Written without recursion: nvcc evaluated the
+// recursive form at run time (CALL + local-memory frames, 8% of k_wsieve's instructions).
+__host__ __device__ constexpr uint32_t wheel_tab_sq(int j) { return 2 * std_prime(j) * std_prime(j); }
+__host__ __device__ constexpr uint32_t wheel_tab_base(int j)
 {
-	return j <= kWheelFirst ? kWtTab : wheel_tab_base(j - 1) + 2 * std_prime(j - 1) * std_prime(j - 1);
+	return kWtTab + (j > 3 ? wheel_tab_sq(3) : 0) + (j > 4 ? wheel_tab_sq(4) : 0) + (j > 5 ? wheel_tab_sq(5) : 0) +
+	       (j > 6 ? wheel_tab_sq(6) : 0) + (j > 7 ? wheel_tab_sq(7) : 0);
 }
+static_assert(kWheelFirst == 3 && kWheelReg == 8, "wheel_tab_base lists the table probes 3..7");
 constexpr uint32_t kWtWords = wheel_tab_base(kWheelReg);
 constexpr uint32_t kWtBytes = (4 * kWtWords + 15) / 16 * 16;  // the per-warp blocks after them stay 16-byte aligned
 #ifndef CGPU_WHEEL_THREADS
