@@ -181,10 +181,10 @@ constexpr uint32_t kWbLists = kWbQueue + 4 * kWheelQueue;
 constexpr uint32_t kWbCls = kWbLists + 2 * 192;
 constexpr uint32_t kWbHist = (kWbCls + 2 * kWheelCls + 15) / 16 * 16;
 __host__ __device__ constexpr uint32_t wheel_warp_bytes(uint32_t np) { return (kWbHist + 4 * np + 15) / 16 * 16; }
-constexpr uint32_t kDefaultRowCostWheel = 160000;  // units of 1/64 instruction (1800 instructions counted; sweep: 2500 best)
-// launches whose mean row has fewer 32-q windows keep k_sieve (TRIANGLE p <= 5e4, mean 780: k_sieve 0.19 ms,
-// k_wsieve 0.25; C4, mean 1.6k: 0.52 / 0.50; 5e4 < p <= 1.5e5, mean 3.1k: 0.86 / 0.59; C5, mean 6.3k: 3.02 / 1.55)
-constexpr uint32_t kWheelMinWindows = 1500;
+constexpr uint32_t kDefaultRowCostWheel = 130000;  // units of 1/64 instruction (~2000 instructions; sweeps r02w/r02x)
+// launches whose mean row has fewer 32-q windows keep k_sieve (TRIANGLE p <= 3e4, mean 470: k_sieve 0.097 ms,
+// k_wsieve 0.117; p <= 5e4, mean 780: 0.189 / 0.175; C4, mean 1.6k: 0.52 / 0.33; C5, mean 6.3k: 3.02 / 1.10)
+constexpr uint32_t kWheelMinWindows = 650;
 constexpr float kDefaultWheelCost[4] = {140.0f, 14.0f, 30.0f, 25.0f};
 
 struct SieveArgs {

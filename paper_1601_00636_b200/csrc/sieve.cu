@@ -889,7 +889,7 @@ struct WheelSmem {
 	uint4* deep;      // [kDeepPrefetch] {row base, r, m, -}
 	uint16_t* cls;    // [kWheelCls] alive classes of the current batch: offsets o < 2431 (q = qa + o + 2431 i)
 	uint16_t* l143;   // [192] alive offsets mod 143 at [0, 143), mod 17 at [160, 177)
-	uint4* fac;       // [kMaxFactors] loop factors {f, barrett m, -(2431^-1) mod f (f < 37681), bit pattern}
+	uint4* fac;       // [kMaxFactors] loop factors {-f, barrett m, -(2431^-1) mod f (f < 37681), bit pattern}
 	const uint32_t* tab;  // the CTA's wheel tables
 	uint32_t tab0;        // ... as a shared address
 };
@@ -1107,20 +1107,23 @@ __device__ __forceinline__ uint32_t wheel_row(const SieveArgs& a, const WheelSme
 				// (q0 mod f) g mod f; pattern = period-f mask below 32, a single bit above
 #pragma unroll 1
 				for (uint32_t s = 0; s < nmid; ++s) {  // (not unrolled: 1.7 factors on average, code size)
-					const uint4 e = w.fac[s];  // {f, m, g, pattern}
-					nonc |= shl_clamp(e.w, mod_full(mod_lazy(q0, e.x, e.y) * e.z, e.x, e.y));
+					const uint4 e = w.fac[s];  // {-f, m, g, pattern}: x + umulhi(x, m) (-f) is the lazy remainder
+					const uint32_t t = (q0 + __umulhi(q0, e.y) * e.x) * e.z;
+					const uint32_t v = t + __umulhi(t, e.y) * e.x;
+					nonc |= shl_clamp(e.w, min(v, v + e.x));
 				}
 #pragma unroll 1
 				for (uint32_t s = nmid; s < nfl; ++s) {  // f >= 37681: at most two multiples of f in [q0, q0 + 31 * 2431]
 					const uint4 e = w.fac[s];
-					const uint32_t t = mod_full(q0, e.x, e.y);
-					uint32_t d = t ? e.x - t : 0u;
+					const uint32_t f = 0u - e.x;
+					const uint32_t t = mod_full(q0, f, e.y);
+					uint32_t d = t ? f - t : 0u;
 #pragma unroll
 					for (int rep = 0; rep < 2; ++rep) {
 						const uint32_t i = __umulhi(min(d, kWheelChunk), kWheelDivMul);
 						nonc |= i * kWheelM == d ? shl_clamp(1u, i) : 0u;
-						d += e.x;
-						if (d < e.x) d = kWheelChunk + 1;  // wrapped past 2^32: no further multiple in reach
+						d += f;
+						if (d < f) d = kWheelChunk + 1;  // wrapped past 2^32: no further multiple in reach
 					}
 				}
 				alive = ~nonc;
@@ -1285,7 +1288,7 @@ __global__ void __launch_bounds__(kWheelThreads, 1) k_wsieve(const SieveArgs a)
 				const uint32_t i17 = (1 + fw * w.tab[kWtNinv17 + fw % 17]) / 17;
 				x = fw - mod_full(i143 * i17, fw, fmv);
 			}
-			w.fac[__popc(keepm & ((1u << lane) - 1))] = make_uint4(fw, fmv, x, fw < 32 ? c_period_mask[fw] : 1u);
+			w.fac[__popc(keepm & ((1u << lane) - 1))] = make_uint4(0u - fw, fmv, x, fw < 32 ? c_period_mask[fw] : 1u);
 		}
 		const uint32_t nmid = __popc(__ballot_sync(kFull, keep && fw < kWheelMidMax));
 		const uint32_t nfl = __popc(keepm);
