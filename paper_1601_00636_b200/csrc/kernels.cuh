@@ -178,7 +178,7 @@ constexpr uint32_t kWheelCls = CGPU_WHEEL_CLS;  // per-warp list of alive classe
 constexpr uint32_t kWbFac = 16 * 8;                          // after uint4 deep[kDeepPrefetch = 8]
 constexpr uint32_t kWbQueue = kWbFac + 16 * kMaxFactors;
 constexpr uint32_t kWbLists = kWbQueue + 4 * kWheelQueue;
-constexpr uint32_t kWbCls = kWbLists + 2 * 192;
+constexpr uint32_t kWbCls = kWbLists + 2 * 192 + 4 * 12;     // lists, then every odd factor (uint32 x kMaxFactors, padded)
 constexpr uint32_t kWbHist = (kWbCls + 2 * kWheelCls + 15) / 16 * 16;
 __host__ __device__ constexpr uint32_t wheel_warp_bytes(uint32_t np) { return (kWbHist + 4 * np + 15) / 16 * 16; }
 constexpr uint32_t kDefaultRowCostWheel = 130000;  // units of 1/64 instruction (~2000 instructions; sweeps r02w/r02x)

@@ -889,6 +889,7 @@ struct WheelSmem {
 	uint4* deep;      // [kDeepPrefetch] {row base, r, m, -}
 	uint16_t* cls;    // [kWheelCls] alive classes of the current batch: offsets o < 2431 (q = qa + o + 2431 i)
 	uint16_t* l143;   // [192] alive offsets mod 143 at [0, 143), mod 17 at [160, 177)
+	uint32_t* allfac; // [kMaxFactors] every odd prime factor of p that can divide a q of the row
 	uint4* fac;       // [kMaxFactors] loop factors {-f, barrett m, -(2431^-1) mod f (f < 37681), bit pattern}
 	const uint32_t* tab;  // the CTA's wheel tables
 	uint32_t tab0;        // ... as a shared address
@@ -925,7 +926,7 @@ __device__ __forceinline__ void wheel_counts(const RowCtx& rc, const WheelSmem& 
 	for (uint32_t sub = lane; sub < (1u << F); sub += 32) {
 		uint64_t d = (rc.even && ((sub >> rc.nf) & 1)) ? 2 : 1;
 		for (uint32_t i = 0; i < rc.nf; ++i)
-			if ((sub >> i) & 1) d *= rc.fac[i];
+			if ((sub >> i) & 1) d *= w.allfac[i];
 		if (d > qb) continue;
 		const uint32_t dd = static_cast<uint32_t>(d);
 		const uint32_t t1 = qb / dd, t0 = (qa - 1) / dd + 1;
@@ -1213,6 +1214,7 @@ __global__ void __launch_bounds__(kWheelThreads, 1) k_wsieve(const SieveArgs a)
 	w.fac = reinterpret_cast<uint4*>(blk + kWbFac);
 	w.queue = reinterpret_cast<uint32_t*>(blk + kWbQueue);
 	w.l143 = reinterpret_cast<uint16_t*>(blk + kWbLists);
+	w.allfac = reinterpret_cast<uint32_t*>(blk + kWbLists + 2 * 192);
 	w.cls = reinterpret_cast<uint16_t*>(blk + kWbCls);
 	w.hist = reinterpret_cast<uint32_t*>(blk + kWbHist);
 	w.tab = s_tab;
@@ -1271,11 +1273,9 @@ __global__ void __launch_bounds__(kWheelThreads, 1) k_wsieve(const SieveArgs a)
 		rc.w0 = unit_window_mult(a, u0, head >> 16, rc.wlast + 1);
 		rc.w1 = unit_window_mult(a, u1, head >> 16, rc.wlast + 1);
 		if (rc.w1 <= rc.w0) continue;
-#pragma unroll
-		for (int k = 0; k < kMaxFactors; ++k) {
-			rc.fac[k] = __shfl_sync(kFull, fw, k + 1);
-			rc.fm[k] = __shfl_sync(kFull, fw, k + 1 + kMaxFactors);
-		}
+		// all odd factors for the analytic counts (wheel_counts reads them from shared memory: lane
+		// L = 1..nf holds factor L - 1)
+		if (lane >= 1 && lane <= rc.nf) w.allfac[lane - 1] = fw;
 		// the loop's factor slots: odd factors other than 11, 13, 17 (lane L = 1..nf holds factor L - 1)
 		const uint32_t fmv = __shfl_down_sync(kFull, fw, kMaxFactors);  // lane L: its Barrett constant
 		const bool keep = lane >= 1 && lane <= rc.nf && fw != 11 && fw != 13 && fw != 17;

@@ -64,6 +64,18 @@ for mode, lo, hi, q0 in cases:
     for i, v in enumerate(rows):
         want[(lo + i) // 100] = max(want.get((lo + i) // 100, 0), int(v))
     assert {r.block_lo + i: int(v) for i, v in enumerate(r.block_rmax) if v} == want
+# a set that ends at 37: no deep probes at all, every q alive after the window loop survives
+P2 = odd_primes(11)
+assert P2[-1] == 37
+tb2, offs2 = port.build_set(P2)
+dev.load(P2, tb2)
+for mode, lo, hi in ((N.TRIANGLE, 2, 2600), (N.REGION, 152, 330)):
+    o = port.sieve(tb2, P2, offs2, lo, hi, mode)
+    r = dev.sieve(lo, hi, mode, surv_cap=1 << 22)
+    assert dev.sieve_kernel() == "k_wsieve"
+    assert (r.pairs_tested, r.survivors) == (o["pairs_tested"], o["survivors"]) and r.survivors > 100
+    assert r.hist.tolist() == o["hist"].tolist()
+    assert np.array_equal(r.survivor_pairs, o["survivor_pairs"])
 print("wheel rows ok", len(cases))
 '''
     env = dict(os.environ, CUBOID_WHEEL="2", ROOT=ROOT)
