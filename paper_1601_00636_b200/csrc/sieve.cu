@@ -1036,6 +1036,7 @@ __device__ __forceinline__ uint32_t wheel_row(const SieveArgs& a, const WheelSme
 		const uint32_t x11 = mod_full(qa11 + c, 11, barrett_m(11)), x13 = mod_full(qa13 + c, 13, barrett_m(13));
 		const bool ok = c < 143 && !((kill11 >> x11) & 1u) && !((kill13 >> x13) & 1u);
 		const uint32_t bal = __ballot_sync(kFull, ok);
+		CGPU_CHECK(n143 + __popc(bal) <= 143);
 		if (ok) w.l143[n143 + __popc(bal & lt)] = static_cast<uint16_t>(c);
 		n143 += __popc(bal);
 	}
@@ -1069,6 +1070,7 @@ __device__ __forceinline__ uint32_t wheel_row(const SieveArgs& a, const WheelSme
 			o = mod_full(w.l143[i143] * kWheelE143 + w.l143[160 + i17] * kWheelE17, kWheelM, barrett_m(kWheelM));
 		const bool ok = ci < cend && o <= span;
 		const uint32_t bal = __ballot_sync(kFull, ok);
+		CGPU_CHECK(n + __popc(bal) <= kWheelCls);
 		if (ok) w.cls[n + __popc(bal & lt)] = static_cast<uint16_t>(o);
 		n += __popc(bal);
 	}
@@ -1142,6 +1144,7 @@ __device__ __forceinline__ uint32_t wheel_row(const SieveArgs& a, const WheelSme
 					const uint32_t r = std_prime(j);
 					const uint32_t rem = mod_lazy(q0, r, barrett_m(r));  // [0, 2r): the rows are doubled
 					uint32_t M;
+					CGPU_CHECK(rem < 2 * r && ta[j - kWheelFirst] + 4 * rem < w.tab0 + 4 * kWtWords);
 					asm volatile("ld.shared.u32 %0, [%1];" : "=r"(M) : "r"(ta[j - kWheelFirst] + 4 * rem));
 					alive &= ~M;
 					if (j + 1 < kWheelReg) S[j + 1 - kWheelFirst] += __popc(alive);
