@@ -1071,7 +1071,9 @@ __device__ __forceinline__ uint32_t wheel_row(const SieveArgs& a, const WheelSme
 		const bool ok = ci < cend && o <= span;
 		const uint32_t bal = __ballot_sync(kFull, ok);
 		CGPU_CHECK(n + __popc(bal) <= kWheelCls);
-		if (ok) w.cls[n + __popc(bal & lt)] = static_cast<uint16_t>(o);
+		// bits 14..15: for even p, 1 + parity of the class's q (q0 + 2431 i alternates parity and the
+		// windows of a class are 77792 q apart): the even q are (entry >> 14) * 0x55555555
+		if (ok) w.cls[n + __popc(bal & lt)] = static_cast<uint16_t>(o | (rc.even ? (1u + ((qa + o) & 1u)) << 14 : 0u));
 		n += __popc(bal);
 	}
 	__syncwarp();
@@ -1084,7 +1086,6 @@ __device__ __forceinline__ uint32_t wheel_row(const SieveArgs& a, const WheelSme
 			const uint32_t r = std_prime(j);
 			ta[j - kWheelFirst] = w.tab0 + 4 * (wheel_tab_base(j) + mod_full(rc.p, r, barrett_m(r)) * 2 * r);
 		}
-		const uint32_t evenm = rc.even ? 0x55555555u : 0u;  // q0 + 2431 i alternates parity
 		const uint32_t nchunk = span / kWheelChunk + 1;
 		const uint32_t total = n * nchunk;
 		const uint32_t n_iter = (total + 31) / 32;
@@ -1103,9 +1104,10 @@ __device__ __forceinline__ uint32_t wheel_row(const SieveArgs& a, const WheelSme
 			const bool last = left == 0;
 			uint32_t alive = 0, q0 = 0;
 			if (!last) {
-				const uint32_t c = w.cls[ci];
+				const uint32_t ce = w.cls[ci];
+				const uint32_t c = ce & 0x3fffu;
 				q0 = qa + c + kWheelChunk * k;
-				uint32_t nonc = evenm << (q0 & 1u);
+				uint32_t nonc = (ce >> 14) * 0x55555555u;
 				// factors below 37681 (ascending, so they come first): the first i with f | q0 + 2431 i is
 				// (q0 mod f) g mod f; pattern = period-f mask below 32, a single bit above
 #pragma unroll 1
@@ -1139,13 +1141,15 @@ __device__ __forceinline__ uint32_t wheel_row(const SieveArgs& a, const WheelSme
 					alive &= vm;
 				}
 				S[0] += __popc(alive);
+				const uint32_t q4 = q0 << 2;
 #pragma unroll
 				for (int j = kWheelFirst; j < kWheelReg; ++j) {
 					const uint32_t r = std_prime(j);
-					const uint32_t rem = mod_lazy(q0, r, barrett_m(r));  // [0, 2r): the rows are doubled
+					// 4 x the lazy remainder (in [0, 8r): the rows are doubled), exact mod 2^32
+					const uint32_t rem4 = q4 - __umulhi(q0, barrett_m(r)) * (4 * r);
 					uint32_t M;
-					CGPU_CHECK(rem < 2 * r && ta[j - kWheelFirst] + 4 * rem < w.tab0 + 4 * kWtWords);
-					asm volatile("ld.shared.u32 %0, [%1];" : "=r"(M) : "r"(ta[j - kWheelFirst] + 4 * rem));
+					CGPU_CHECK(rem4 < 8 * r && ta[j - kWheelFirst] + rem4 < w.tab0 + 4 * kWtWords);
+					asm volatile("ld.shared.u32 %0, [%1];" : "=r"(M) : "r"(ta[j - kWheelFirst] + rem4));
 					alive &= ~M;
 					if (j + 1 < kWheelReg) S[j + 1 - kWheelFirst] += __popc(alive);
 				}
