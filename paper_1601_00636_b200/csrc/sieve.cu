@@ -1098,12 +1098,11 @@ __device__ __forceinline__ uint32_t wheel_row(const SieveArgs& a, const WheelSme
 		}
 
 		// `left` counts the iterations down; the last n_edge of them touch the row's partial windows
-		// or lanes past the end, and one more pass drains what is left in the queue
+		// or lanes past the end
 		const uint32_t n_edge = n_iter - n_full;
-		for (uint32_t left = n_iter;; --left) {
-			const bool last = left == 0;
-			uint32_t alive = 0, q0 = 0;
-			if (!last) {
+		for (uint32_t left = n_iter; left; --left) {
+			uint32_t alive, q0;
+			{
 				const uint32_t ce = w.cls[ci];
 				const uint32_t c = ce & 0x3fffu;
 				q0 = qa + c + kWheelChunk * k;
@@ -1160,27 +1159,30 @@ __device__ __forceinline__ uint32_t wheel_row(const SieveArgs& a, const WheelSme
 				}
 			}
 			uint32_t m = __ballot_sync(kFull, alive != 0);
-			do {
-				if (m) {
-					CGPU_CHECK(qn + __popc(m) <= kWheelQueue);
-					if (alive) {
-						const uint32_t bit = __ffs(alive) - 1;
-						w.queue[qn + __popc(m & lt)] = q0 + kWheelM * bit;
-						alive &= alive - 1;
-					}
-					qn += __popc(m);
+			while (m) {  // usually one pass: a second only for a lane with two q alive
+				CGPU_CHECK(qn + __popc(m) <= kWheelQueue);
+				if (alive) {
+					const uint32_t bit = __ffs(alive) - 1;
+					w.queue[qn + __popc(m & lt)] = q0 + kWheelM * bit;
+					alive &= alive - 1;
 				}
-				if (qn >= 32 || (last && qn)) {
-					const uint32_t nd = min(qn, 32u);
+				qn += __popc(m);
+				if (qn >= 32) {
 					__syncwarp();
-					qn -= nd;
-					entered += nd;
-					wheel_drain(a, w, lane, qn, nd, rc.p, kmax);
+					qn -= 32;
+					entered += 32;
+					wheel_drain(a, w, lane, qn, 32, rc.p, kmax);
 					__syncwarp();
 				}
 				m = __ballot_sync(kFull, alive != 0);
-			} while (m);
-			if (last) break;
+			}
+		}
+		if (qn) {  // what the batch leaves
+			__syncwarp();
+			entered += qn;
+			wheel_drain(a, w, lane, 0, qn, rc.p, kmax);
+			qn = 0;
+			__syncwarp();
 		}
 	}
 	__syncwarp();
