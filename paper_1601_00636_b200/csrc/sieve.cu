@@ -1416,7 +1416,15 @@ __global__ void k_wheeltab(const uint32_t* __restrict__ ext, const WheelTabArgs 
 			int j = kWheelFirst;
 			while (j + 1 < kWheelReg && e >= wheel_tab_base(j + 1)) ++j;
 			const uint32_t r = std_prime(j), i = e - wheel_tab_base(j), a = i / (2 * r), b = i % (2 * r);
-			for (uint32_t l = 0; l < 32; ++l) v |= ubit(j, a, (b + kWheelM * l) % r) << l;
+			// the row's words once (r <= 37: at most two hold bits below r), then 32 bits at stride 2431 mod r
+			const uint32_t* row = ext + t.base[j] + a * ext_row_words(r);
+			const uint32_t w0 = row[0], w1 = row[1];
+			uint32_t x = b % r;
+			for (uint32_t l = 0; l < 32; ++l) {
+				v |= (((x < 32 ? w0 : w1) >> (x & 31)) & 1u) << l;
+				x += kWheelM % r;
+				if (x >= r) x -= r;
+			}
 		}
 		out[e] = v;
 	}
