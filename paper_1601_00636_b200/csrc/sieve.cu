@@ -247,6 +247,16 @@ __device__ __forceinline__ uint32_t factorise_chunk(const SieveArgs& a, PlanSmem
 	__syncthreads();
 	if (c0 + t >= a.n_slots) return 0;
 	uint32_t nf = 0, even = 0;
+	// gathered while the factors are found (re-reading them from `out` afterwards waited on global memory):
+	// the coprime share of the odd factors, and k_wsieve's loop factors by path
+	float cop_odd = 1.0f;
+	uint32_t nmid = 0, nlarge = 0;
+	auto note_factor = [&](uint32_t f) {
+		cop_odd -= cop_odd * __frcp_rn(static_cast<float>(f));
+		if (f == a.reg_r[0] || f == a.reg_r[1] || f == a.reg_r[2]) return;  // the wheel primes drop classes instead
+		if (f < kWheelMidMax) ++nmid;
+		else ++nlarge;
+	};
 	if (rb.qhi >= rb.qlo && rb.p > 1) {
 		const uint32_t n = min(sm.nf[t], static_cast<uint32_t>(kMaxFactors));
 		uint16_t f[kMaxFactors];
@@ -270,6 +280,7 @@ __device__ __forceinline__ uint32_t factorise_chunk(const SieveArgs& a, PlanSmem
 			} else if (fp.x <= rb.qhi && nf < kMaxFactors) {
 				out[1 + kMaxFactors + nf] = fp.y;
 				out[1 + nf++] = fp.x;
+				note_factor(fp.x);
 			}
 		}
 		if (cof > 1) {  // the prime factor above sqrt(p)
@@ -278,17 +289,18 @@ __device__ __forceinline__ uint32_t factorise_chunk(const SieveArgs& a, PlanSmem
 			} else if (cof <= rb.qhi && nf < kMaxFactors) {
 				out[1 + kMaxFactors + nf] = static_cast<uint32_t>((1ull << 32) / cof);
 				out[1 + nf++] = cof;
+				note_factor(cof);
 			}
 		}
 	}
 	out[0] = nf | (even << 8);
 	// window weight (row_units): survival after the register probes that do
 	// not divide p, times the row's coprime candidates per window
-	float surv = 1.0f, cop = even ? 0.5f : 1.0f;
+	float surv = 1.0f;
+	const float cop = (even ? 0.5f : 1.0f) * cop_odd;
 	const uint32_t p32 = static_cast<uint32_t>(rb.p);
 	for (uint32_t j = 0; j < a.nreg; ++j)
 		if (mod_full(p32, a.reg_r[j], a.reg_m[j])) surv *= 1.0f - sm.kill[j];
-	for (uint32_t j = 0; j < nf; ++j) cop -= cop * __frcp_rn(static_cast<float>(out[1 + j]));
 	if (a.wheel) {
 		// k_wsieve: instructions of the row's loop = iterations x (base + per factor) + queued q x
 		// drain cost, spread over the row's windows in units of 1/64 instruction (16 bits). The
@@ -301,13 +313,6 @@ __device__ __forceinline__ uint32_t factorise_chunk(const SieveArgs& a, PlanSmem
 			for (uint32_t j = 0; j < static_cast<uint32_t>(kWheelFirst); ++j) {
 				const float r = static_cast<float>(a.reg_r[j]);
 				classes *= mod_full(p32, a.reg_r[j], a.reg_m[j]) ? rintf(r * (1.0f - sm.kill[j])) : r - 1.0f;
-			}
-			uint32_t nmid = 0, nlarge = 0;
-			for (uint32_t j = 0; j < nf; ++j) {
-				const uint32_t f = out[1 + j];
-				if (f == a.reg_r[0] || f == a.reg_r[1] || f == a.reg_r[2]) continue;
-				if (f < kWheelMidMax) ++nmid;
-				else ++nlarge;
 			}
 			const float q = static_cast<float>(wn) * 32.0f;
 			const float nchunk = floorf((q - 1.0f) * (1.0f / kWheelChunk)) + 1.0f;
